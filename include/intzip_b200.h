@@ -1,0 +1,174 @@
+/*
+ * intzip_b200.h — C ABI of the B200-native SIMD-BP128 / SIMD-FastPFOR decoder.
+ *
+ * This is the drop-in boundary for the hot path of the reference library
+ * `intzip` (arXiv 1209.2137): the decode side of
+ *
+ *   intzip::decode_array(const Codec&, std::span<const Chunk>, std::vector<uint32_t>&)
+ *       /root/reference/proj/core/include/intzip/codec.h:64-71
+ *       /root/reference/proj/core/src/codec.cpp:39-76
+ *   intzip::Codec::decode_deltas(std::span<const uint32_t>, uint32_t*, size_t)
+ *       /root/reference/proj/core/include/intzip/codec.h:36-40
+ *
+ * for the codecs "simdbp128", "simdbp128-s4", "simdfastpfor", "simdfastpfor-s4"
+ * (registry: /root/reference/proj/core/src/codec.cpp:85-109).  The compressed
+ * word format is the reference's, unchanged, so chunks
+ * encoded by the CPU reference decode here and vice versa.
+ *
+ * The reference has no FFI of its own (it is a C++ library); every entry point
+ * below replaces one reference call and names it.  All signatures use plain
+ * pointers and sizes.  Device entry points are stream-ordered and never
+ * synchronise or allocate; host entry points (suffix _host) are synchronous.
+ * There is no CPU fallback: without a usable sm_100a device every compute
+ * entry point returns IZG_ERR_NO_DEVICE.
+ */
+#ifndef INTZIP_B200_H
+#define INTZIP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Chunk length cap: intzip::kChunkSize (codec.h:17). */
+#define IZG_CHUNK_SIZE 65536u
+
+/* Codec formats on the hot path (codec_binpack.h:17-25, codec_patched.h:69-85). */
+typedef enum izg_codec {
+  IZG_SIMDBP128 = 0,
+  IZG_SIMDFASTPFOR = 1
+} izg_codec;
+
+/* Inverse differential coding fused into decode.
+ *   NONE : no prefix sum; Codec::decode_deltas semantics (codec.h:36-40).
+ *   D1   : DeltaMode::scalar  x_i = x_{i-1} + d_i          (delta.cpp:25-51)
+ *   D4   : DeltaMode::stride4 x_i = x_{i-4} + d_i          (delta.cpp:60-75)
+ *   D2, DM : EXTENSIONS, not in the reference (delta.h:22 has only scalar and
+ *          stride4).  D2: x_i = x_{i-2} + d_i; DM: x_{4k+j} = x_{4k-1} + d_{4k+j}
+ *          (x_{-1} = 0).  Parity unpinned.              */
+typedef enum izg_delta {
+  IZG_DELTA_NONE = 0,
+  IZG_DELTA_D1 = 1,
+  IZG_DELTA_D4 = 2,
+  IZG_DELTA_D2 = 3,
+  IZG_DELTA_DM = 4
+} izg_delta;
+
+/* One independently decodable chunk (intzip::Chunk, codec.h:54-57) placed in a
+ * word buffer.  `n` is Chunk::original_length, `n_words` is payload.size(). */
+typedef struct izg_chunk {
+  uint64_t word_off; /* index of the first payload word in the word buffer */
+  uint32_t n_words;  /* payload words                                     */
+  uint32_t n;        /* decoded integers (1..65536 for array semantics)   */
+  uint64_t out_off;  /* index of the first decoded integer in the output  */
+} izg_chunk;
+
+/* Per-chunk status.  Every nonzero code mirrors one reference throw site; a
+ * host wrapper maps 1..63 to intzip::CorruptError and 64.. to
+ * std::invalid_argument, as the reference would have thrown. */
+typedef enum izg_status {
+  IZG_OK = 0,
+  /* pipeline, codec.cpp */
+  IZG_E_CHUNK_LENGTH = 1,      /* codec.cpp:43-44   chunk: bad original length      */
+  IZG_E_PAYLOAD_SIZE = 2,      /* codec.cpp:63-64   chunk: payload size mismatch    */
+  /* Variable Byte remainder, codec_basic.cpp */
+  IZG_E_VBYTE_TRUNCATED = 3,   /* codec_basic.cpp:34-35 vbyte: truncated stream     */
+  IZG_E_VBYTE_OVERFLOW = 4,    /* codec_basic.cpp:38-39 vbyte: value exceeds 32 bits*/
+  IZG_E_VBYTE_TOO_LONG = 5,    /* codec_basic.cpp:43-44 vbyte: longer than 5 bytes  */
+  /* SIMD-BP128, codec_binpack.cpp */
+  IZG_E_BP_TRUNC_DESC = 6,     /* codec_binpack.cpp:101-102 truncated descriptor    */
+  IZG_E_BP_WIDTH = 7,          /* codec_binpack.cpp:110-111 width byte exceeds 32   */
+  IZG_E_BP_TRUNC_PAYLOAD = 8,  /* codec_binpack.cpp:112-113 truncated payload       */
+  /* SIMD-FastPFOR, codec_patched.cpp */
+  IZG_E_FP_TRUNC_PAGE = 9,     /* codec_patched.cpp:298     truncated page          */
+  IZG_E_FP_BA_OFFSET = 10,     /* codec_patched.cpp:300-301 bad byte-array offset   */
+  IZG_E_FP_TRUNC_BA = 11,      /* codec_patched.cpp:304-305 truncated byte array    */
+  IZG_E_FP_TRUNC_META = 12,    /* codec_patched.cpp:313-314,321-322 truncated block metadata */
+  IZG_E_FP_WIDTHS = 13,        /* codec_patched.cpp:318-319 bad block widths        */
+  IZG_E_FP_EMPTY_EXC = 14,     /* codec_patched.cpp:324     empty exception list    */
+  IZG_E_FP_TRUNC_POS = 15,     /* codec_patched.cpp:325-326 truncated positions     */
+  IZG_E_FP_POS_RANGE = 16,     /* codec_patched.cpp:328-330 position out of range   */
+  IZG_E_FP_BA_LEN = 17,        /* codec_patched.cpp:335-336 byte array length mismatch */
+  IZG_E_FP_NO_BITSET = 18,     /* codec_patched.cpp:347-348 missing exception bitset*/
+  IZG_E_FP_TRUNC_EXC = 19,     /* codec_patched.cpp:352-353,362-363 truncated exception array */
+  IZG_E_FP_OVERRUN = 20,       /* codec_patched.cpp:387-388 packed blocks overrun   */
+  IZG_E_FP_EXHAUSTED = 21,     /* codec_patched.cpp:406-407 exception array exhausted */
+  IZG_E_FP_PACKED_SIZE = 22,   /* codec_patched.cpp:414-415 packed area size mismatch */
+  /* misuse -> std::invalid_argument */
+  IZG_E_COUNT_MULTIPLE = 64,   /* codec_binpack.cpp:13-14, codec_patched.cpp:53-54 count % 128 != 0 */
+  IZG_E_PAGE_TOO_LARGE = 65    /* codec_patched.cpp:55-56 page exceeds 65536 integers */
+} izg_status;
+
+/* API-level return codes (not per chunk). */
+#define IZG_SUCCESS 0
+#define IZG_ERR_INVALID_ARGUMENT (-1) /* bad enum, null pointer, misaligned buffer */
+#define IZG_ERR_CUDA (-2)             /* a CUDA runtime call failed               */
+#define IZG_ERR_NO_DEVICE (-3)        /* no sm_100 device: there is no CPU fallback */
+#define IZG_ERR_CORRUPT (-4)          /* _host calls: some chunk had status != 0  */
+#define IZG_ERR_UNKNOWN_CODEC (-5)    /* make_codec: unknown codec (codec.cpp:108) */
+
+/* ---- library --------------------------------------------------------- */
+
+/* Human-readable text of a per-chunk status (the reference's what()). */
+const char* izg_status_string(int32_t status);
+
+/* make_codec(name) (codec.cpp:99-109) restricted to the hot-path codecs:
+ * "simdbp128" -> (IZG_SIMDBP128, D1), "simdbp128-s4" -> (.., D4), likewise
+ * "simdfastpfor[-s4]".  Extension names "-d2"/"-dm" select D2/DM.  Returns
+ * IZG_SUCCESS or IZG_ERR_UNKNOWN_CODEC. */
+int izg_parse_codec_name(const char* name, int* codec, int* delta);
+
+/* Word-buffer placement contract for izg_decode: the buffer is 16-byte
+ * aligned, and for every chunk the 16-byte-aligned span covering its payload
+ * lies inside the allocation.  izg_layout_chunks assigns word_off for chunks
+ * of the given sizes (SIMD-BP128 payloads start 16-byte aligned, SIMD-FastPFOR
+ * pages start at 12 mod 16 so their packed rows are 16-byte aligned) and
+ * returns the total words to allocate (trailing pad included). */
+uint64_t izg_layout_chunks(int codec, const uint32_t* n_words, uint32_t n_chunks,
+                           uint64_t* word_off_out);
+
+/* ---- device entry points (stream-ordered) ---------------------------- */
+
+/* Fused decode of a batch of chunks, one kernel launch.
+ *   delta == IZG_DELTA_NONE : per chunk, Codec::decode_deltas(payload, out, n)
+ *                             (codec.h:36-40): n % 128 == 0 required; words
+ *                             consumed go to d_consumed[i] (nullable).
+ *   otherwise               : per chunk, the body of decode_array's chunk loop
+ *                             (codec.cpp:50-68): core decode, Variable Byte
+ *                             remainder, exact-consumption check, prefix sum.
+ * d_status[i] receives the chunk's izg_status (0 = OK); after a nonzero
+ * status the chunk's output is unspecified (delta.h:19-20).  d_words must
+ * follow izg_layout_chunks's contract.  stream is a cudaStream_t (NULL =
+ * legacy default stream).  Returns IZG_SUCCESS or an API error. */
+int izg_decode(int codec, int delta, const uint32_t* d_words,
+               const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
+               int32_t* d_status, uint32_t* d_consumed, void* stream);
+
+/* Order-sensitive checksum of n words: sum over i of (w_i + 1) * (2i + 1)
+ * mod 2^64 (xor of all words in d_result[1]).  Used for whole-box parity with
+ * an NCCL reduction; not part of the reference. */
+int izg_checksum(const uint32_t* d_data, uint64_t n, uint64_t* d_result,
+                 void* stream);
+
+/* ---- host entry points (synchronous, host buffers) -------------------- */
+
+/* decode_array over a batch of chunks held in HOST memory: copies the words
+ * and chunk table to the device, decodes, copies the integers back.  h_status
+ * (nullable, n_chunks entries) receives per-chunk statuses; returns
+ * IZG_ERR_CORRUPT if any chunk failed.  Device scratch is cached per thread
+ * and grown on demand. */
+int izg_decode_host(int codec, int delta, const uint32_t* h_words,
+                    uint64_t n_words, const izg_chunk* h_chunks,
+                    uint32_t n_chunks, uint32_t* h_out, uint64_t n_out,
+                    int32_t* h_status);
+
+/* Release the per-thread device scratch used by the _host entry points. */
+void izg_release_host_scratch(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* INTZIP_B200_H */

@@ -1,0 +1,395 @@
+"""ctypes access to the parity checkers.  TEST INFRASTRUCTURE ONLY.
+
+* ``Oracle``    — oracle/_build/liboracle.so, the C restatement (intzip_oracle.c)
+* ``Reference`` — oracle/_ref/libintzip_ref.so, the reference library compiled
+                  from /root/reference/proj/core/src by oracle/Makefile
+
+Only tests/, __graft_entry__.smoke() and bench.py's reference / cpu_baseline
+legs import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libintzip_ref.so")
+
+CHUNK_DTYPE = np.dtype([("word_off", "<u8"), ("n_words", "<u4"), ("n", "<u4"),
+                        ("out_off", "<u8")])
+CODECS = {"simdbp128": (0, 1), "simdbp128-s4": (0, 2), "simdfastpfor": (1, 1),
+          "simdfastpfor-s4": (1, 2), "simdbp128-d2": (0, 3), "simdbp128-dm": (0, 4),
+          "simdfastpfor-d2": (1, 3), "simdfastpfor-dm": (1, 4)}
+
+
+def build() -> None:
+    """Compile the oracle (and the reference shim where the sources exist)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _p(a):
+    return a.ctypes.data
+
+
+class Oracle:
+    """The C restatement; statuses are izg_status codes."""
+
+    def __init__(self):
+        if not os.path.exists(ORACLE_SO):
+            build()
+        self.L = L = C.CDLL(ORACLE_SO)
+        vp, sz = C.c_void_p, C.c_size_t
+        L.orc_max_bitwidth.restype = C.c_uint32
+        L.orc_max_bitwidth.argtypes = [vp, sz]
+        L.orc_unpack_vertical128.argtypes = [vp, C.c_uint32, vp]
+        L.orc_pack_vertical128.argtypes = [vp, C.c_uint32, vp]
+        L.orc_delta_decode.argtypes = [C.c_int, vp, sz]
+        L.orc_delta_encode.restype = C.c_int
+        L.orc_delta_encode.argtypes = [C.c_int, vp, sz, C.c_int]
+        L.orc_vbyte_encode.restype = sz
+        L.orc_vbyte_encode.argtypes = [vp, sz, vp]
+        L.orc_vbyte_decode.restype = C.c_int
+        L.orc_vbyte_decode.argtypes = [vp, sz, vp, sz, C.POINTER(sz)]
+        L.orc_histogram_of_widths.argtypes = [vp, sz, vp]
+        L.orc_fastpfor_cost_bits.restype = C.c_uint64
+        L.orc_fastpfor_cost_bits.argtypes = [vp, C.c_uint32, C.c_uint32]
+        L.orc_fastpfor_choose_width.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint32),
+                                                C.POINTER(C.c_uint32)]
+        L.orc_encode_bound.restype = sz
+        L.orc_encode_bound.argtypes = [C.c_int, sz]
+        L.orc_encode_deltas.restype = sz
+        L.orc_encode_deltas.argtypes = [C.c_int, vp, sz, vp]
+        L.orc_decode_deltas.restype = C.c_int
+        L.orc_decode_deltas.argtypes = [C.c_int, vp, sz, vp, sz, C.POINTER(sz)]
+        L.orc_encode_chunk.restype = sz
+        L.orc_encode_chunk.argtypes = [C.c_int, C.c_int, vp, C.c_uint32, vp, C.c_int]
+        L.orc_decode_chunk.restype = C.c_int
+        L.orc_decode_chunk.argtypes = [C.c_int, C.c_int, vp, sz, C.c_uint32, vp]
+
+    def max_bitwidth(self, v):
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        return self.L.orc_max_bitwidth(_p(v), len(v))
+
+    def unpack_vertical128(self, words, b):
+        words = np.ascontiguousarray(words, dtype=np.uint32)
+        out = np.zeros(128, dtype=np.uint32)
+        self.L.orc_unpack_vertical128(_p(words), b, _p(out))
+        return out
+
+    def pack_vertical128(self, values, b):
+        values = np.ascontiguousarray(values, dtype=np.uint32)
+        out = np.zeros(max(4 * b, 1), dtype=np.uint32)
+        self.L.orc_pack_vertical128(_p(values), b, _p(out))
+        return out[:4 * b]
+
+    def delta_decode(self, delta, v):
+        v = np.array(v, dtype=np.uint32)
+        self.L.orc_delta_decode(delta, _p(v), len(v))
+        return v
+
+    def delta_encode(self, delta, v, allow_wrap=False):
+        v = np.array(v, dtype=np.uint32)
+        if self.L.orc_delta_encode(delta, _p(v), len(v), int(allow_wrap)):
+            raise ValueError("delta encode: input is not nondecreasing")
+        return v
+
+    def vbyte_encode(self, v):
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        out = np.zeros(5 * len(v) + 1, dtype=np.uint8)
+        n = self.L.orc_vbyte_encode(_p(v), len(v), _p(out))
+        return out[:n]
+
+    def vbyte_decode(self, b, count):
+        b = np.ascontiguousarray(b, dtype=np.uint8)
+        out = np.zeros(max(count, 1), dtype=np.uint32)
+        used = C.c_size_t()
+        st = self.L.orc_vbyte_decode(_p(b), len(b), _p(out), count, C.byref(used))
+        return st, out[:count], used.value
+
+    def choose_width(self, hist33, block_len):
+        h = np.ascontiguousarray(hist33, dtype=np.uint32)
+        b, m = C.c_uint32(), C.c_uint32()
+        self.L.orc_fastpfor_choose_width(_p(h), block_len, C.byref(b), C.byref(m))
+        return b.value, m.value
+
+    def cost_bits(self, hist33, block_len, b):
+        h = np.ascontiguousarray(hist33, dtype=np.uint32)
+        return self.L.orc_fastpfor_cost_bits(_p(h), block_len, b)
+
+    def histogram(self, v):
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        h = np.zeros(33, dtype=np.uint32)
+        self.L.orc_histogram_of_widths(_p(v), len(v), _p(h))
+        return h
+
+    def encode_deltas(self, name, deltas):
+        codec = CODECS[name][0]
+        deltas = np.ascontiguousarray(deltas, dtype=np.uint32)
+        out = np.zeros(self.L.orc_encode_bound(codec, len(deltas)) + 64, dtype=np.uint32)
+        n = self.L.orc_encode_deltas(codec, _p(deltas), len(deltas), _p(out))
+        if n == C.c_size_t(-1).value:
+            raise ValueError("count")
+        return out[:n]
+
+    def decode_deltas(self, name, words, count):
+        codec = CODECS[name][0]
+        words = np.ascontiguousarray(words, dtype=np.uint32)
+        out = np.zeros(max(count, 1), dtype=np.uint32)
+        used = C.c_size_t()
+        st = self.L.orc_decode_deltas(codec, _p(words) if len(words) else None, len(words),
+                                      _p(out), count, C.byref(used))
+        return st, out[:count], used.value
+
+    def encode_chunk(self, name, values, allow_wrap=False):
+        codec, delta = CODECS[name]
+        values = np.ascontiguousarray(values, dtype=np.uint32)
+        out = np.zeros(self.L.orc_encode_bound(codec, len(values)) + 256, dtype=np.uint32)
+        n = self.L.orc_encode_chunk(codec, delta, _p(values), len(values), _p(out),
+                                    int(allow_wrap))
+        if n == C.c_size_t(-1).value:
+            raise ValueError("delta encode: input is not nondecreasing")
+        return out[:n]
+
+    def decode_chunk(self, name, payload, n):
+        codec, delta = CODECS[name]
+        payload = np.ascontiguousarray(payload, dtype=np.uint32)
+        out = np.zeros(max(n, 1), dtype=np.uint32)
+        st = self.L.orc_decode_chunk(codec, delta, _p(payload) if len(payload) else None,
+                                     len(payload), n, _p(out))
+        return st, out[:n]
+
+    def encode_array(self, name, values, allow_wrap=False):
+        values = np.ascontiguousarray(values, dtype=np.uint32)
+        return [(min(65536, len(values) - o),
+                 self.encode_chunk(name, values[o:o + 65536], allow_wrap))
+                for o in range(0, len(values), 65536)]
+
+    def decode_array(self, name, chunks):
+        outs = []
+        for n, payload in chunks:
+            st, out = self.decode_chunk(name, payload, n)
+            if st:
+                return st, None
+            outs.append(out)
+        return 0, (np.concatenate(outs) if outs else np.zeros(0, np.uint32))
+
+
+class RefError(Exception):
+    def __init__(self, code, what):
+        self.code, self.what = code, what
+        super().__init__(f"[{code}] {what}")
+
+
+class Reference:
+    """The reference library itself (compiled from source); raises RefError
+    with code 1 (CorruptError), 2 (invalid_argument) or 3 (other)."""
+
+    def __init__(self):
+        if not os.path.exists(REF_SO):
+            build()
+        if not os.path.exists(REF_SO):
+            raise FileNotFoundError(REF_SO)
+        self.L = L = C.CDLL(REF_SO)
+        vp, u64, u32 = C.c_void_p, C.c_uint64, C.c_uint32
+        cp = C.c_char_p
+        L.izr_encode_array.restype = C.c_int
+        L.izr_encode_array.argtypes = [cp, vp, u64, vp, u64, vp, u32, C.POINTER(u64),
+                                       C.POINTER(u32), C.c_char_p, C.c_int]
+        L.izr_encode_chunk_wrapping.restype = C.c_int
+        L.izr_encode_chunk_wrapping.argtypes = [cp, vp, u32, vp, u64, C.POINTER(u64), C.c_char_p,
+                                                C.c_int]
+        L.izr_decode_array.restype = C.c_int
+        L.izr_decode_array.argtypes = [cp, vp, vp, u32, vp, u64, C.c_char_p, C.c_int]
+        L.izr_encode_deltas.restype = C.c_int
+        L.izr_encode_deltas.argtypes = [cp, vp, u64, vp, u64, C.POINTER(u64), C.c_char_p, C.c_int]
+        L.izr_decode_deltas.restype = C.c_int
+        L.izr_decode_deltas.argtypes = [cp, vp, u64, vp, u64, C.POINTER(u64), C.c_char_p, C.c_int]
+        L.izr_unpack_vertical128.restype = C.c_int
+        L.izr_unpack_vertical128.argtypes = [vp, u32, vp]
+        L.izr_pack_vertical128.restype = C.c_int
+        L.izr_pack_vertical128.argtypes = [vp, u32, vp, C.c_int]
+        L.izr_max_bitwidth.restype = u32
+        L.izr_max_bitwidth.argtypes = [vp, u64]
+        L.izr_delta.restype = C.c_int
+        L.izr_delta.argtypes = [C.c_int, C.c_int, vp, u64]
+        L.izr_vbyte_encode.restype = C.c_int
+        L.izr_vbyte_encode.argtypes = [vp, u64, vp, C.POINTER(u64)]
+        L.izr_vbyte_decode.restype = C.c_int
+        L.izr_vbyte_decode.argtypes = [vp, u64, vp, u64, C.POINTER(u64), C.c_char_p, C.c_int]
+        L.izr_choose_width.restype = C.c_int
+        L.izr_choose_width.argtypes = [vp, u32, C.POINTER(u32), C.POINTER(u32), C.POINTER(u64)]
+        L.izr_gen.restype = C.c_int
+        L.izr_gen.argtypes = [C.c_int, u64, u64, u64, vp]
+        L.izr_batch_create.restype = vp
+        L.izr_batch_create.argtypes = [cp, vp, vp, u32]
+        L.izr_batch_decode.restype = C.c_double
+        L.izr_batch_decode.argtypes = [vp, u32, u32, C.c_int]
+        L.izr_batch_output.restype = C.c_int
+        L.izr_batch_output.argtypes = [vp, u32, vp]
+        L.izr_batch_free.restype = None
+        L.izr_batch_free.argtypes = [vp]
+
+    @staticmethod
+    def _check(rc, err):
+        if rc:
+            raise RefError(rc, err.value.decode())
+
+    def encode_array(self, name, values):
+        values = np.ascontiguousarray(values, dtype=np.uint32)
+        nchunks = (len(values) + 65535) // 65536
+        cap = 2 * len(values) + 1024 * (nchunks + 1)
+        words = np.zeros(cap, dtype=np.uint32)
+        table = np.zeros(max(nchunks, 1), dtype=CHUNK_DTYPE)
+        nw, nc = C.c_uint64(), C.c_uint32()
+        err = C.create_string_buffer(256)
+        rc = self.L.izr_encode_array(name.encode(), _p(values), len(values), _p(words), cap,
+                                     _p(table), len(table), C.byref(nw), C.byref(nc), err, 256)
+        self._check(rc, err)
+        table = table[:nc.value]
+        return [(int(t["n"]), words[int(t["word_off"]):int(t["word_off"]) + int(t["n_words"])].copy())
+                for t in table]
+
+    def encode_chunk_wrapping(self, name, values):
+        values = np.ascontiguousarray(values, dtype=np.uint32)
+        cap = 2 * len(values) + 1024
+        words = np.zeros(cap, dtype=np.uint32)
+        nw = C.c_uint64()
+        err = C.create_string_buffer(256)
+        rc = self.L.izr_encode_chunk_wrapping(name.encode(), _p(values), len(values), _p(words),
+                                              cap, C.byref(nw), err, 256)
+        self._check(rc, err)
+        return words[:nw.value].copy()
+
+    def decode_array(self, name, chunks):
+        """chunks: list of (n, payload); raises RefError like decode_array."""
+        payloads = [np.ascontiguousarray(p, dtype=np.uint32) for _, p in chunks]
+        words = np.concatenate(payloads) if payloads else np.zeros(1, np.uint32)
+        if len(words) == 0:
+            words = np.zeros(1, np.uint32)
+        table = np.zeros(max(len(chunks), 1), dtype=CHUNK_DTYPE)
+        off = 0
+        for i, (n, p) in enumerate(chunks):
+            table[i] = (off, len(p), n, 0)
+            off += len(p)
+        total = sum(n for n, _ in chunks)
+        out = np.zeros(max(total, 1), dtype=np.uint32)
+        err = C.create_string_buffer(256)
+        rc = self.L.izr_decode_array(name.encode(), _p(words), _p(table), len(chunks), _p(out),
+                                     len(out), err, 256)
+        self._check(rc, err)
+        return out[:total]
+
+    def encode_deltas(self, name, deltas):
+        deltas = np.ascontiguousarray(deltas, dtype=np.uint32)
+        cap = 2 * len(deltas) + 1024
+        words = np.zeros(cap, dtype=np.uint32)
+        nw = C.c_uint64()
+        err = C.create_string_buffer(256)
+        rc = self.L.izr_encode_deltas(name.encode(), _p(deltas), len(deltas), _p(words), cap,
+                                      C.byref(nw), err, 256)
+        self._check(rc, err)
+        return words[:nw.value].copy()
+
+    def decode_deltas(self, name, words, count):
+        words = np.ascontiguousarray(words, dtype=np.uint32)
+        buf = words if len(words) else np.zeros(1, np.uint32)
+        out = np.zeros(max(count, 1), dtype=np.uint32)
+        used = C.c_uint64()
+        err = C.create_string_buffer(256)
+        rc = self.L.izr_decode_deltas(name.encode(), _p(buf), len(words), _p(out), count,
+                                      C.byref(used), err, 256)
+        self._check(rc, err)
+        return out[:count], used.value
+
+    def unpack_vertical128(self, words, b):
+        words = np.ascontiguousarray(words, dtype=np.uint32)
+        buf = words if len(words) else np.zeros(4, np.uint32)
+        out = np.zeros(128, dtype=np.uint32)
+        if self.L.izr_unpack_vertical128(_p(buf), b, _p(out)):
+            raise RefError(2, "width")
+        return out
+
+    def pack_vertical128(self, values, b, masked=False):
+        values = np.ascontiguousarray(values, dtype=np.uint32)
+        out = np.zeros(4 * 33, dtype=np.uint32)
+        rc = self.L.izr_pack_vertical128(_p(values), b, _p(out), int(masked))
+        if rc:
+            raise RefError(rc, "pack")
+        return out[:4 * b]
+
+    def max_bitwidth(self, v):
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        return self.L.izr_max_bitwidth(_p(v) if len(v) else None, len(v))
+
+    def delta(self, encode, stride4, v):
+        v = np.array(v, dtype=np.uint32)
+        buf = v if len(v) else np.zeros(1, np.uint32)
+        rc = self.L.izr_delta(int(encode), int(stride4), _p(buf), len(v))
+        if rc:
+            raise RefError(rc, "delta")
+        return buf[:len(v)]
+
+    def vbyte_encode(self, v):
+        v = np.ascontiguousarray(v, dtype=np.uint32)
+        out = np.zeros(5 * len(v) + 1, dtype=np.uint8)
+        n = C.c_uint64()
+        self.L.izr_vbyte_encode(_p(v) if len(v) else None, len(v), _p(out), C.byref(n))
+        return out[:n.value]
+
+    def vbyte_decode(self, b, count):
+        b = np.ascontiguousarray(b, dtype=np.uint8)
+        buf = b if len(b) else np.zeros(1, np.uint8)
+        out = np.zeros(max(count, 1), dtype=np.uint32)
+        used = C.c_uint64()
+        err = C.create_string_buffer(256)
+        rc = self.L.izr_vbyte_decode(_p(buf), len(b), _p(out), count, C.byref(used), err, 256)
+        self._check(rc, err)
+        return out[:count], used.value
+
+    def choose_width(self, hist33, block_len):
+        h = np.ascontiguousarray(hist33, dtype=np.uint32)
+        b, m, c = C.c_uint32(), C.c_uint32(), C.c_uint64()
+        self.L.izr_choose_width(_p(h), block_len, C.byref(b), C.byref(m), C.byref(c))
+        return b.value, m.value, c.value
+
+    def gen(self, model, n, rng, seed):
+        out = np.zeros(max(n, 1), dtype=np.uint32)
+        if self.L.izr_gen({"uniform": 0, "cluster": 1}[model], n, rng, seed, _p(out)):
+            raise RefError(2, "gen")
+        return out[:n]
+
+    # ---- timed batch decode (reference arm / cpu_baseline) ----
+    def batch(self, name, words, table):
+        words = np.ascontiguousarray(words, dtype=np.uint32)
+        table = np.ascontiguousarray(table, dtype=CHUNK_DTYPE)
+        return RefBatch(self, self.L.izr_batch_create(name.encode(), _p(words), _p(table),
+                                                      len(table)), len(table))
+
+
+class RefBatch:
+    def __init__(self, ref, handle, n):
+        self.ref, self.h, self.n = ref, handle, n
+
+    def decode(self, first=0, count=None, threads=1) -> float:
+        count = self.n - first if count is None else count
+        t = self.ref.L.izr_batch_decode(self.h, first, count, threads)
+        if t < 0:
+            raise RefError(1, "decode failed in batch")
+        return t
+
+    def output(self, i, n):
+        out = np.zeros(n, dtype=np.uint32)
+        self.ref.L.izr_batch_output(self.h, i, _p(out))
+        return out
+
+    def close(self):
+        if self.h:
+            self.ref.L.izr_batch_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

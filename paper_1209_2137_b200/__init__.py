@@ -1,0 +1,14 @@
+"""B200-native fused SIMD-BP128 / SIMD-FastPFOR decoder (arXiv 1209.2137 hot path).
+
+The product is libintzip_b200.so (paper_1209_2137_b200/_lib), whose C ABI is
+include/intzip_b200.h; this package is its Python face (ctypes).
+"""
+from . import _native
+from .codec import (CHUNK_SIZE, Codec, CorruptError, Encoded, codec_names, decode_array,
+                    encode_array, encode_chunks, gen_arrays, layout, make_codec,
+                    raise_for_status)
+from .device import DeviceBatch
+
+__all__ = ["CHUNK_SIZE", "Codec", "CorruptError", "DeviceBatch", "Encoded", "codec_names",
+           "decode_array", "encode_array", "encode_chunks", "gen_arrays", "layout",
+           "make_codec", "raise_for_status", "_native"]

@@ -1,0 +1,186 @@
+"""Python mirror of the reference codec interface for the hot path.
+
+Mirrors ``intzip::Codec`` / ``make_codec`` / ``encode_array`` /
+``decode_array`` (/root/reference/proj/core/include/intzip/codec.h:23-77) so
+parity tests read like the reference's own tests.  Decoding always runs the
+fused sm_100a kernel through the C ABI (include/intzip_b200.h); encoding runs
+the host encoder mirror of libintzip_b200.  Errors: ``CorruptError`` where the
+reference throws ``intzip::CorruptError`` (errors.h:8-14), ``ValueError``
+where it throws ``std::invalid_argument``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from ._native import CHUNK_DTYPE
+
+CHUNK_SIZE = 1 << 16  # kChunkSize (codec.h:17)
+DELTA_NAMES = {N.DELTA_NONE: "none", N.DELTA_D1: "scalar", N.DELTA_D4: "stride4",
+               N.DELTA_D2: "stride2(ext)", N.DELTA_DM: "max4(ext)"}
+
+
+class CorruptError(RuntimeError):
+    """intzip::CorruptError (errors.h:8-14): malformed compressed input."""
+
+    def __init__(self, status: int, chunk: int | None = None):
+        self.status = int(status)
+        self.chunk = chunk
+        where = "" if chunk is None else f" (chunk {chunk})"
+        super().__init__(N.status_string(status) + where)
+
+
+def raise_for_status(status: int, chunk: int | None = None) -> None:
+    if status == 0:
+        return
+    if status >= 64:  # std::invalid_argument sites
+        raise ValueError(N.status_string(status))
+    raise CorruptError(status, chunk)
+
+
+@dataclass(frozen=True)
+class Codec:
+    """intzip::Codec (codec.h:23-52) for simdbp128[-s4] / simdfastpfor[-s4]."""
+    name: str
+    codec: int
+    delta: int
+    block_multiple: int = 128  # codec_binpack.cpp:64-66, codec_patched.cpp:216-217
+
+    @property
+    def delta_mode(self) -> str:
+        return DELTA_NAMES[self.delta]
+
+
+def make_codec(name: str) -> Codec:
+    """make_codec (codec.cpp:99-109); unknown names raise ValueError."""
+    c, d = C.c_int(), C.c_int()
+    rc = N.lib().izg_parse_codec_name(name.encode(), C.byref(c), C.byref(d))
+    if rc != N.SUCCESS:
+        raise ValueError(f"unknown codec: {name}")
+    return Codec(name, c.value, d.value)
+
+
+def codec_names() -> list[str]:
+    """The hot-path subset of codec_names() (codec.cpp:111-119)."""
+    return ["simdbp128", "simdbp128-s4", "simdfastpfor", "simdfastpfor-s4"]
+
+
+@dataclass
+class Encoded:
+    """Chunks of one or more arrays laid out for the device (izg_layout_chunks)."""
+    words: np.ndarray  # uint32, 16-byte-aligned placement contract
+    table: np.ndarray  # CHUNK_DTYPE
+
+    @property
+    def n_out(self) -> int:
+        if len(self.table) == 0:
+            return 0
+        return int((self.table["out_off"] + self.table["n"]).max())
+
+    @property
+    def payload_words(self) -> int:
+        return int(self.table["n_words"].sum())
+
+
+def _threads() -> int:
+    return max(1, min(64, os.cpu_count() or 1))
+
+
+def encode_chunks(codec: Codec, values: np.ndarray, value_off: np.ndarray,
+                  counts: np.ndarray, *, allow_wrap: bool = False, raw: bool = False,
+                  threads: int | None = None) -> Encoded:
+    """Host-encode independent chunks values[value_off[i] : +counts[i]].
+
+    raw=True encodes deltas as-is (Codec::encode_deltas, codec.h:31-34);
+    allow_wrap=True takes differences mod 2^32.
+    """
+    L = N.lib()
+    values = np.ascontiguousarray(values, dtype=np.uint32)
+    value_off = np.ascontiguousarray(value_off, dtype=np.uint64)
+    counts = np.ascontiguousarray(counts, dtype=np.uint32)
+    st = C.c_int()
+    delta = N.DELTA_NONE if raw else codec.delta
+    h = L.izg_encode_batch_host(codec.codec, delta, N.ptr(values), N.ptr(value_off),
+                                N.ptr(counts), len(counts), int(allow_wrap),
+                                threads or _threads(), C.byref(st))
+    if not h:
+        raise ValueError("encode: invalid input (decreasing values or bad counts)")
+    try:
+        nw = L.izg_encoded_words(h)
+        words = np.empty(nw, dtype=np.uint32)
+        table = np.empty(len(counts), dtype=CHUNK_DTYPE)
+        L.izg_encoded_copy(h, N.ptr(words), N.ptr(table), threads or _threads())
+    finally:
+        L.izg_encoded_free(h)
+    return Encoded(words, table)
+
+
+def encode_array(codec: Codec, values, *, allow_wrap: bool = False) -> Encoded:
+    """encode_array (codec.cpp:14-37): chunks of 2^16, delta, core, VByte tail."""
+    values = np.ascontiguousarray(values, dtype=np.uint32)
+    n = len(values)
+    offs = np.arange(0, n, CHUNK_SIZE, dtype=np.uint64)
+    counts = np.minimum(CHUNK_SIZE, n - offs).astype(np.uint32)
+    return encode_chunks(codec, values, offs, counts, allow_wrap=allow_wrap)
+
+
+def layout(codec: Codec, payloads: list[np.ndarray], counts, out_offs=None) -> Encoded:
+    """Place existing chunk payloads (e.g. from the CPU reference) for the device."""
+    sizes = np.array([len(p) for p in payloads], dtype=np.uint32)
+    offs = np.empty(len(payloads), dtype=np.uint64)
+    total = N.lib().izg_layout_chunks(codec.codec, N.ptr(sizes), len(payloads), N.ptr(offs))
+    words = np.zeros(total, dtype=np.uint32)
+    for p, o in zip(payloads, offs):
+        words[int(o):int(o) + len(p)] = p
+    table = np.empty(len(payloads), dtype=CHUNK_DTYPE)
+    table["word_off"] = offs
+    table["n_words"] = sizes
+    table["n"] = np.asarray(counts, dtype=np.uint32)
+    if out_offs is None:
+        out_offs = np.concatenate([[0], np.cumsum(table["n"].astype(np.uint64))[:-1]])
+    table["out_off"] = out_offs
+    return Encoded(words, table)
+
+
+def decode_array(codec: Codec, enc: Encoded, *, raw: bool = False,
+                 return_status: bool = False):
+    """decode_array (codec.cpp:39-76) through the GPU, host buffers in and out.
+
+    Raises CorruptError / ValueError with the first failing chunk's status
+    (the reference throws at the first failing chunk) unless return_status.
+    """
+    L = N.lib()
+    n_out = enc.n_out
+    out = np.zeros(max(n_out, 1), dtype=np.uint32)
+    status = np.zeros(max(len(enc.table), 1), dtype=np.int32)
+    delta = N.DELTA_NONE if raw else codec.delta
+    rc = L.izg_decode_host(codec.codec, delta, N.ptr(enc.words), len(enc.words),
+                           N.ptr(enc.table), len(enc.table), N.ptr(out), len(out),
+                           N.ptr(status))
+    if rc not in (N.SUCCESS, N.ERR_CORRUPT):
+        raise RuntimeError(f"izg_decode_host failed: {rc}")
+    status = status[:len(enc.table)]
+    if return_status:
+        return out[:n_out], status
+    bad = np.nonzero(status)[0]
+    if len(bad):
+        raise_for_status(int(status[bad[0]]), int(bad[0]))
+    return out[:n_out]
+
+
+def gen_arrays(model: str, count: int, n: int, d, seed: int, *, rate_ppm: int = 0,
+               threads: int | None = None):
+    """Seeded synthetic arrays (izg_gen_arrays); returns (values[count, n], d[count])."""
+    models = {"uniform": 0, "cluster": 1, "geometric": 2, "raw": 3}
+    d_lo, d_hi = (d, d) if np.isscalar(d) else d
+    out = np.empty((count, n), dtype=np.uint32)
+    dd = np.empty(count, dtype=np.uint32)
+    rc = N.lib().izg_gen_arrays(models[model], count, n, d_lo, d_hi, seed, rate_ppm,
+                                threads or _threads(), N.ptr(out), N.ptr(dd))
+    if rc != N.SUCCESS:
+        raise ValueError("gen_arrays: bad arguments")
+    return out, dd

@@ -1,0 +1,240 @@
+// host.cpp — host half of the C ABI: codec registry mirror, status strings,
+// buffer placement, and the synchronous host-buffer decode (the end-to-end
+// entry point a user of decode_array would call).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string_view>
+#include <vector>
+
+#include "../../include/intzip_b200.h"
+
+extern "C" const char* izg_status_string(int32_t s) {
+  switch (s) {
+    case IZG_OK: return "ok";
+    case IZG_E_CHUNK_LENGTH: return "chunk: bad original length";
+    case IZG_E_PAYLOAD_SIZE: return "chunk: payload size mismatch";
+    case IZG_E_VBYTE_TRUNCATED: return "vbyte: truncated stream";
+    case IZG_E_VBYTE_OVERFLOW: return "vbyte: value exceeds 32 bits";
+    case IZG_E_VBYTE_TOO_LONG: return "vbyte: integer longer than 5 bytes";
+    case IZG_E_BP_TRUNC_DESC: return "simdbp128: truncated descriptor";
+    case IZG_E_BP_WIDTH: return "simdbp128: width byte exceeds 32";
+    case IZG_E_BP_TRUNC_PAYLOAD: return "simdbp128: truncated payload";
+    case IZG_E_FP_TRUNC_PAGE: return "fastpfor: truncated page";
+    case IZG_E_FP_BA_OFFSET: return "fastpfor: bad byte-array offset";
+    case IZG_E_FP_TRUNC_BA: return "fastpfor: truncated byte array";
+    case IZG_E_FP_TRUNC_META: return "fastpfor: truncated block metadata";
+    case IZG_E_FP_WIDTHS: return "fastpfor: bad block widths";
+    case IZG_E_FP_EMPTY_EXC: return "fastpfor: empty exception list";
+    case IZG_E_FP_TRUNC_POS: return "fastpfor: truncated exception positions";
+    case IZG_E_FP_POS_RANGE: return "fastpfor: exception position out of range";
+    case IZG_E_FP_BA_LEN: return "fastpfor: byte array length mismatch";
+    case IZG_E_FP_NO_BITSET: return "fastpfor: missing exception bitset";
+    case IZG_E_FP_TRUNC_EXC: return "fastpfor: truncated exception array";
+    case IZG_E_FP_OVERRUN: return "fastpfor: packed blocks overrun byte array";
+    case IZG_E_FP_EXHAUSTED: return "fastpfor: exception array exhausted";
+    case IZG_E_FP_PACKED_SIZE: return "fastpfor: packed area size mismatch";
+    case IZG_E_COUNT_MULTIPLE: return "count must be a multiple of 128";
+    case IZG_E_PAGE_TOO_LARGE: return "patched codec: page exceeds 65536 integers";
+    default: return "unknown status";
+  }
+}
+
+// make_codec (codec.cpp:99-109) for the hot-path codecs; "-d2"/"-dm" are
+// the D2/DM extensions (not in the reference registry).
+extern "C" int izg_parse_codec_name(const char* name, int* codec, int* delta) {
+  if (!name || !codec || !delta) return IZG_ERR_INVALID_ARGUMENT;
+  std::string_view s(name);
+  int d = IZG_DELTA_D1;
+  auto strip = [&](std::string_view suf, int mode) {
+    if (s.size() >= suf.size() && s.substr(s.size() - suf.size()) == suf) {
+      s.remove_suffix(suf.size());
+      d = mode;
+      return true;
+    }
+    return false;
+  };
+  strip("-s4", IZG_DELTA_D4) || strip("-d2", IZG_DELTA_D2) || strip("-dm", IZG_DELTA_DM);
+  if (s == "simdbp128")
+    *codec = IZG_SIMDBP128;
+  else if (s == "simdfastpfor")
+    *codec = IZG_SIMDFASTPFOR;
+  else
+    return IZG_ERR_UNKNOWN_CODEC;
+  *delta = d;
+  return IZG_SUCCESS;
+}
+
+extern "C" uint64_t izg_layout_chunks(int codec, const uint32_t* n_words, uint32_t n_chunks,
+                                      uint64_t* word_off_out) {
+  // SIMD-BP128 payload word 0 on a 16-byte boundary (codec_binpack.h:17-23);
+  // SIMD-FastPFOR page word 0 at 12 mod 16 so packed rows (word 1 + 4k,
+  // codec_patched.cpp:225,250-253) are 16-byte aligned.
+  const uint64_t phase = codec == IZG_SIMDFASTPFOR ? 3 : 0;
+  uint64_t pos = 0;
+  for (uint32_t i = 0; i < n_chunks; ++i) {
+    pos = (pos + 3 - phase) / 4 * 4 + phase;
+    if (pos < phase) pos = phase;
+    word_off_out[i] = pos;
+    pos += n_words[i];
+  }
+  return (pos + 3) / 4 * 4 + 4;  // whole 16-byte rows plus one spare row
+}
+
+// ---- synchronous host-buffer decode -----------------------------------
+
+namespace {
+
+constexpr int kSlots = 3;
+
+struct Slot {
+  cudaStream_t stream = nullptr;
+  uint32_t* words = nullptr;
+  uint64_t words_cap = 0;
+  izg_chunk* table = nullptr;
+  uint32_t table_cap = 0;
+  uint32_t* out = nullptr;
+  uint64_t out_cap = 0;
+  int32_t* status = nullptr;
+};
+
+struct Scratch {
+  int device = -1;
+  Slot slot[kSlots];
+  std::vector<int32_t> status_host;
+  void release() {
+    for (auto& s : slot) {
+      if (s.words) cudaFree(s.words);
+      if (s.table) cudaFree(s.table);
+      if (s.out) cudaFree(s.out);
+      if (s.status) cudaFree(s.status);
+      if (s.stream) cudaStreamDestroy(s.stream);
+      s = Slot{};
+    }
+    device = -1;
+  }
+  ~Scratch() { release(); }
+};
+
+thread_local Scratch t_scratch;
+
+template <class T>
+bool grow(T*& p, uint64_t& cap, uint64_t need) {
+  if (need <= cap) return true;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  const uint64_t n = std::max<uint64_t>(need, 1024);
+  if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return false;
+  cap = n;
+  return true;
+}
+
+}  // namespace
+
+extern "C" void izg_release_host_scratch(void) { t_scratch.release(); }
+
+// Pipelined over pieces of the chunk table on three streams, so the
+// host->device copy of piece k+1, the decode of piece k and the device->host
+// copy of piece k-1 overlap (separate copy engines).  Chunks must be ordered
+// by word_off and out_off (as encode_array / izg_layout_chunks produce);
+// otherwise the whole batch is one piece.
+extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, uint64_t n_words,
+                               const izg_chunk* h_chunks, uint32_t n_chunks, uint32_t* h_out,
+                               uint64_t n_out, int32_t* h_status) {
+  if (n_chunks == 0) return IZG_SUCCESS;
+  if (!h_words || !h_chunks || !h_out) return IZG_ERR_INVALID_ARGUMENT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return IZG_ERR_NO_DEVICE;
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Scratch& S = t_scratch;
+  if (S.device != dev) {
+    S.release();
+    S.device = dev;
+    for (auto& s : S.slot)
+      if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess)
+        return IZG_ERR_CUDA;
+  }
+  // Validate the table against the host buffers (bounds of the copies).
+  bool ordered = true;
+  for (uint32_t i = 0; i < n_chunks; ++i) {
+    const izg_chunk& c = h_chunks[i];
+    if (c.word_off + c.n_words > n_words || c.out_off + c.n > n_out)
+      return IZG_ERR_INVALID_ARGUMENT;
+    if (i && (c.word_off < h_chunks[i - 1].word_off || c.out_off < h_chunks[i - 1].out_off))
+      ordered = false;
+  }
+  // Pieces of about 32 MiB of output.
+  std::vector<uint32_t> cuts{0};
+  if (ordered) {
+    uint64_t acc = 0;
+    for (uint32_t i = 0; i < n_chunks; ++i) {
+      acc += h_chunks[i].n;
+      if (acc >= (uint64_t{8} << 20) && i + 1 < n_chunks) {
+        cuts.push_back(i + 1);
+        acc = 0;
+      }
+    }
+  }
+  cuts.push_back(n_chunks);
+  S.status_host.assign(h_status ? 0 : n_chunks, 0);
+  int32_t* st_host = h_status ? h_status : S.status_host.data();
+  int rc = IZG_SUCCESS;
+  for (size_t p = 0; p + 1 < cuts.size() && rc == IZG_SUCCESS; ++p) {
+    Slot& s = S.slot[p % kSlots];
+    const uint32_t c0 = cuts[p], c1 = cuts[p + 1], nc = c1 - c0;
+    uint64_t wlo = UINT64_MAX, whi = 0, olo = UINT64_MAX, ohi = 0;
+    for (uint32_t i = c0; i < c1; ++i) {
+      wlo = std::min(wlo, h_chunks[i].word_off);
+      whi = std::max(whi, h_chunks[i].word_off + h_chunks[i].n_words);
+      olo = std::min(olo, h_chunks[i].out_off);
+      ohi = std::max(ohi, h_chunks[i].out_off + h_chunks[i].n);
+    }
+    wlo &= ~uint64_t{3};                              // keep 16-byte alignment
+    const uint64_t wcopy = std::min<uint64_t>(n_words, (whi + 3) & ~uint64_t{3}) - wlo;
+    const uint64_t wneed = ((whi + 3) & ~uint64_t{3}) - wlo + 4;  // + the contract's pad row
+    uint64_t tcap = s.table_cap;
+    if (!grow(s.words, s.words_cap, wneed) || !grow(s.table, tcap, nc) ||
+        !grow(s.out, s.out_cap, std::max<uint64_t>(ohi - olo, 1))) {
+      rc = IZG_ERR_CUDA;
+      break;
+    }
+    s.table_cap = (uint32_t)tcap;
+    if (!s.status) {
+      if (cudaMalloc(&s.status, sizeof(int32_t) * (1u << 20)) != cudaSuccess) {
+        rc = IZG_ERR_CUDA;
+        break;
+      }
+    }
+    if (nc > (1u << 20)) {
+      rc = IZG_ERR_INVALID_ARGUMENT;
+      break;
+    }
+    cudaMemsetAsync(s.words + wcopy, 0, (wneed - wcopy) * 4, s.stream);
+    cudaMemcpyAsync(s.words, h_words + wlo, wcopy * 4, cudaMemcpyHostToDevice, s.stream);
+    cudaMemcpyAsync(s.table, h_chunks + c0, sizeof(izg_chunk) * nc, cudaMemcpyHostToDevice,
+                    s.stream);
+    // Shifted base pointers: the kernel adds the table's absolute offsets.
+    const int r = izg_decode(codec, delta, s.words - wlo, s.table, nc, s.out - olo, s.status,
+                             nullptr, s.stream);
+    if (r != IZG_SUCCESS) {
+      rc = r;
+      break;
+    }
+    cudaMemcpyAsync(h_out + olo, s.out, (ohi - olo) * 4, cudaMemcpyDeviceToHost, s.stream);
+    cudaMemcpyAsync(st_host + c0, s.status, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost,
+                    s.stream);
+  }
+  for (auto& s : S.slot)
+    if (cudaStreamSynchronize(s.stream) != cudaSuccess) rc = IZG_ERR_CUDA;
+  if (rc != IZG_SUCCESS) return rc;
+  for (uint32_t i = 0; i < n_chunks; ++i)
+    if (st_host[i] != IZG_OK) return IZG_ERR_CORRUPT;
+  return IZG_SUCCESS;
+}

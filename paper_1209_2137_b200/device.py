@@ -1,0 +1,77 @@
+"""Device-resident batches for izg_decode (stream-ordered, no host sync).
+
+torch provides device memory and streams only (plumbing); the decode itself is
+the fused kernel behind the C ABI.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+from .codec import Codec, Encoded, raise_for_status
+
+
+class DeviceBatch:
+    """An Encoded batch resident in HBM plus its output and status buffers."""
+
+    def __init__(self, codec: Codec, enc: Encoded, device=None, *, raw: bool = False):
+        import torch
+
+        self.torch = torch
+        self.codec = codec
+        self.delta = N.DELTA_NONE if raw else codec.delta
+        self.device = torch.device(device or "cuda")
+        self.n_chunks = len(enc.table)
+        self.n_out = enc.n_out
+        self.payload_words = enc.payload_words
+        self.words = torch.from_numpy(enc.words.view(np.int32)).to(self.device)
+        self.table = torch.from_numpy(enc.table.view(np.uint8)).to(self.device)
+        self.out = torch.empty(max(self.n_out, 1), dtype=torch.int32, device=self.device)
+        self.status = torch.full((max(self.n_chunks, 1),), -1, dtype=torch.int32,
+                                 device=self.device)
+        self.consumed = torch.zeros(max(self.n_chunks, 1), dtype=torch.int32,
+                                    device=self.device)
+        self.sums = torch.zeros(2, dtype=torch.int64, device=self.device)
+
+    @property
+    def algorithmic_bytes(self) -> int:
+        """Compressed bytes read + 4 B per decoded integer."""
+        return 4 * self.payload_words + 4 * self.n_out
+
+    def decode(self, stream=None) -> None:
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        rc = N.lib().izg_decode(self.codec.codec, self.delta, N.ptr(self.words),
+                                N.ptr(self.table), self.n_chunks, N.ptr(self.out),
+                                N.ptr(self.status), N.ptr(self.consumed), s.cuda_stream)
+        if rc != N.SUCCESS:
+            raise RuntimeError(f"izg_decode failed: {rc}")
+
+    def checksum(self, stream=None) -> tuple[int, int]:
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        rc = N.lib().izg_checksum(N.ptr(self.out), self.n_out, N.ptr(self.sums), s.cuda_stream)
+        if rc != N.SUCCESS:
+            raise RuntimeError(f"izg_checksum failed: {rc}")
+        v = self.sums.cpu().numpy().view(np.uint64)
+        return int(v[0]), int(v[1])
+
+    def statuses(self) -> np.ndarray:
+        return self.status[:self.n_chunks].cpu().numpy()
+
+    def check(self) -> None:
+        st = self.statuses()
+        bad = np.nonzero(st)[0]
+        if len(bad):
+            raise_for_status(int(st[bad[0]]), int(bad[0]))
+
+    def output(self) -> np.ndarray:
+        return self.out[:self.n_out].cpu().numpy().view(np.uint32)
+
+
+def host_checksum(values: np.ndarray, base_index: int = 0) -> tuple[int, int]:
+    """izg_checksum on the host: sum (w+1)(2i+1) mod 2^64, xor of words."""
+    v = np.ascontiguousarray(values, dtype=np.uint32).reshape(-1).astype(np.uint64)
+    i = np.arange(base_index, base_index + len(v), dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        s = int(np.sum((v + np.uint64(1)) * (np.uint64(2) * i + np.uint64(1)), dtype=np.uint64))
+    x = int(np.bitwise_xor.reduce(v)) if len(v) else 0
+    return s, x

@@ -1,0 +1,48 @@
+"""Developer timing loop: decode throughput of one config (CUDA events)."""
+import sys, os, time, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1209_2137_b200 as P
+
+def run(name, model, count, d, seed=1, rate=0, reps=20, raw=False):
+    codec = P.make_codec(name)
+    t0 = time.time()
+    vals, _ = P.gen_arrays(model, count, 65536, d, seed=seed, rate_ppm=rate)
+    flat = vals.reshape(-1)
+    offs = np.arange(count, dtype=np.uint64) * 65536
+    enc = P.encode_chunks(codec, flat, offs, np.full(count, 65536, np.uint32),
+                          allow_wrap=(model == "geometric"), raw=raw)
+    t1 = time.time()
+    b = P.DeviceBatch(codec, enc, raw=raw)
+    for _ in range(3): b.decode()
+    torch.cuda.synchronize(); b.check()
+    if not raw:
+        from paper_1209_2137_b200.device import host_checksum
+        ok = b.checksum() == host_checksum(flat)
+    else:
+        ok = np.array_equal(b.output()[:65536*4], flat[:65536*4])
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); b.decode(); e1.record(); torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    t = float(np.median(ts))
+    n = count * 65536
+    gb = b.algorithmic_bytes / t / 1e9
+    print(json.dumps(dict(name=name, model=model, d=d, rate=rate, raw=raw, ok=bool(ok),
+        bits_per_int=round(32 * b.payload_words / n, 3), ms=round(t * 1e3, 4),
+        gints=round(n / t / 1e9, 2), alg_GBps=round(gb, 1), frac=round(gb / 6532.9, 3),
+        prep_s=round(t1 - t0, 1))), flush=True)
+
+if __name__ == "__main__":
+    which = sys.argv[1:] or ["c1"]
+    for w in which:
+        if w == "c1": run("simdbp128-s4", "cluster", 1024, 29)
+        if w == "c1big": run("simdbp128-s4", "cluster", 8192, 29)
+        if w == "d1": run("simdbp128", "cluster", 4096, 29)
+        if w == "d4u": run("simdbp128-s4", "uniform", 4096, 26)
+        if w == "c4": run("simdfastpfor-s4", "geometric", 2048, 32, rate=100000)
+        if w == "raw":
+            for b in (0, 8, 16, 24, 32): run("simdbp128", "raw", 4096, b, raw=True)
