@@ -1,10 +1,11 @@
 // decode.cu — fused decode kernels and the izg_decode / izg_checksum C ABI.
 //
-// Kernel shape: persistent CTAs, one producer warp whose lane 0
-// streams each chunk's compressed payload into a 64 KiB shared-memory ring
-// with TMA bulk copies (cp.async.bulk + mbarrier complete_tx), and eight
-// consumer warps that decode straight out of the ring, fuse the prefix sum,
-// and write every decoded integer to HBM exactly once.
+// Kernel shape: persistent CTAs of kWarps independent warps.
+// Each warp claims whole chunks, streams the chunk's compressed payload into
+// its private 8 KiB shared-memory ring with TMA bulk copies (cp.async.bulk +
+// mbarrier complete_tx), decodes straight out of the ring with the prefix sum
+// fused, and writes every decoded integer to HBM exactly once.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -18,16 +19,9 @@
 
 namespace izg {
 
-struct SmemHead {
-  uint64_t full[kNStage];
-  uint64_t empty[kNStage];
-  uint4 tot[2][kCW];
-};
-
-// Per-chunk argument checks every role applies identically before touching
-// the payload: decode_array's length check (codec.cpp:43-44) or
-// decode_deltas' count checks (codec_binpack.cpp:12-15,
-// codec_patched.cpp:52-57).
+// Per-chunk argument checks applied before touching the payload:
+// decode_array's length check (codec.cpp:43-44) or decode_deltas' count
+// checks (codec_binpack.cpp:12-15, codec_patched.cpp:52-57).
 __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t n) {
   if (array_mode) {
     if (n == 0 || n > IZG_CHUNK_SIZE) return IZG_E_CHUNK_LENGTH;
@@ -38,92 +32,84 @@ __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t
   return IZG_OK;
 }
 
+// Persistent kernel: every warp repeatedly claims the next chunk (one atomic
+// per chunk) and decodes it end to end: stream, unpack, patch, prefix sum,
+// VByte remainder, consumption check, status.
 template <int CODEC, int DELTA>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kWarps * 32, 3)
     decode_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                   uint32_t n_chunks, uint32_t* __restrict__ out, int32_t* __restrict__ status,
-                  uint32_t* __restrict__ consumed) {
+                  uint32_t* __restrict__ consumed, uint32_t* __restrict__ next_chunk,
+                  const __grid_constant__ CUtensorMap omap, int tma_out) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* ring = smem;
-  SmemHead* head = reinterpret_cast<SmemHead*>(smem + kRing);
   constexpr bool kArray = DELTA != IZG_DELTA_NONE;
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-
-  if (tid == 0) {
-    for (uint32_t i = 0; i < kNStage; ++i) {
-      mbar_init(&head->full[i], 1);
-      mbar_init(&head->empty[i], 1);
-    }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpRing r;
+  r.gen = smem + warp * kRingBytes;
+  r.base = smem_u32(r.gen);
+  r.full = reinterpret_cast<uint64_t*>(smem + kBarOff) + warp * kNS;
+  OutStage os;
+  os.base = smem_u32(smem + kOutOff + warp * 2 * kStageOut);
+  os.buf = 0;
+  os.tmap = &omap;
+  os.leader = lane == 0;
+  r.g = 0;
+  r.leader = lane == 0;
+  r.policy = policy_evict_first();
+  if (lane == 0) {
+    for (uint32_t i = 0; i < kNS; ++i) mbar_init(&r.full[i], 1);
     fence_barrier_init();
   }
-  __syncthreads();
+  __syncwarp();
 
-  if (warp == kCW) {
-    // ---------------- producer ----------------
-    if ((tid & 31) != 0) return;
-    const uint64_t pol = policy_evict_first();
-    uint32_t g = 0;
-    for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
-      const izg_chunk ch = chunks[c];
-      if (precheck(CODEC, kArray, ch.n) != IZG_OK) continue;
-      const StreamGeom sg = stream_geom(words, ch.word_off, ch.n_words);
-      produce_chunk(ring, head->full, head->empty, sg, g, pol);
-    }
-    return;
-  }
-
-  // ---------------- consumers ----------------
-  uint32_t g = 0, tbuf = 0;
-  for (uint32_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
+  for (;;) {
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(next_chunk, 1u);
+    c = __shfl_sync(0xFFFFFFFFu, c, 0);
+    if (c >= n_chunks) break;
     const izg_chunk ch = chunks[c];
     int32_t st = precheck(CODEC, kArray, ch.n);
-    if (st != IZG_OK) {
-      if (tid == 0) {
-        status[c] = st;
-        if (consumed) consumed[c] = 0;
-      }
-      continue;
-    }
-    const StreamGeom sg = stream_geom(words, ch.word_off, ch.n_words);
-    RingView rv{smem_u32(ring), g, sg.phase, sg.nst, 0, 0};
-    g += sg.nst;
-    uint32_t* o = out + ch.out_off;
-    const bool oal = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
-    const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
-    uint4 carry = make_uint4(0, 0, 0, 0);
     uint32_t pos = 0;
-    if (CODEC == IZG_SIMDBP128) {
-      if (sg.phase == 0)
-        st = bp128_core<DELTA, true>(rv, head->full, head->empty, head->tot, tbuf, ch.n_words,
-                                     core / 128, o, oal, carry, &pos);
-      else
-        st = bp128_core<DELTA, false>(rv, head->full, head->empty, head->tot, tbuf, ch.n_words,
-                                      core / 128, o, oal, carry, &pos);
-    } else {
-      st = fastpfor_core<DELTA>(rv, head->full, head->empty, head->tot, tbuf, ch.n_words,
-                                core / 128, o, oal, carry, &pos);
-    }
-    if (kArray && st == IZG_OK) {
-      if (core < ch.n) {
-        // Variable Byte remainder (codec.cpp:56-62), then exact consumption.
-        rv.ensure(head->full, 4u * ch.n_words);
-        if (tid == 0) {
+    if (st == IZG_OK) {
+      r.begin(words, ch.word_off, ch.n_words);
+      uint32_t* o = out + ch.out_off;
+      const bool oal = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+      const int64_t orow = tma_out && (ch.out_off & 31) == 0 ? (int64_t)(ch.out_off >> 5) : -1;
+      const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
+      uint4 carry = make_uint4(0, 0, 0, 0);
+      if (CODEC == IZG_SIMDBP128) {
+        if (r.phase == 0)
+          st = bp128_core<DELTA, true>(r, os, ch.n_words, core / 128, o, oal, orow, carry, &pos);
+        else
+          st = bp128_core<DELTA, false>(r, os, ch.n_words, core / 128, o, oal, orow, carry,
+                                        &pos);
+      } else {
+        st = fastpfor_core<DELTA>(r, os, words + ch.word_off, ch.n_words, core / 128, o, oal,
+                                  orow, carry, &pos);
+      }
+      if (kArray && st == IZG_OK) {
+        if (core < ch.n) {
+          // Variable Byte remainder (codec.cpp:56-62).
+          r.release_below(4u * pos);
+          r.ensure(4u * ch.n_words);
           uint32_t rb = 0;
-          st = vbyte_tail<DELTA>(rv, 4u * pos, 4u * (ch.n_words - pos), core, ch.n - core, carry,
-                                 o, &rb);
+          if (lane == 0)
+            st = vbyte_tail<DELTA>(r, 4u * pos, 4u * (ch.n_words - pos), core, ch.n - core,
+                                   carry, o, &rb);
+          st = __shfl_sync(0xFFFFFFFFu, st, 0);
+          rb = __shfl_sync(0xFFFFFFFFu, rb, 0);
           if (st == IZG_OK) pos += (rb + 3) / 4;
         }
+        if (st == IZG_OK && pos != ch.n_words) st = IZG_E_PAYLOAD_SIZE;  // codec.cpp:63-64
       }
-      if (tid == 0 && st == IZG_OK && pos != ch.n_words) st = IZG_E_PAYLOAD_SIZE;
+      r.end();
     }
-    named_bar_sync(1, kConsumers);
-    rv.finish(head->full, head->empty, tid == 0);
-    if (tid == 0) {
+    if (lane == 0) {
       status[c] = st;
       if (consumed) consumed[c] = st == IZG_OK ? pos : 0;
     }
   }
+  os.drain();
 }
 
 // ---- checksum ------------------------------------------------------------
@@ -150,10 +136,36 @@ __global__ void checksum_kernel(const uint32_t* __restrict__ d, uint64_t n,
 
 // ---- launch plumbing -------------------------------------------------------
 
-constexpr size_t kSmemBytes = kRing + sizeof(SmemHead);
-
 using KernelFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
-                          uint32_t*);
+                          uint32_t*, uint32_t*, const CUtensorMap, int);
+
+// 2-D view of the output for TMA stores: rows of 32 integers (128 B), box
+// of 16 rows (one warp iteration), 128-byte swizzle.  The row extent is
+// nominal (the kernel only stores rows of real chunks).
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool make_out_map(CUtensorMap* m, uint32_t* out) {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  if (!fn || (reinterpret_cast<uintptr_t>(out) & 127)) return false;
+  const cuuint64_t dims[2] = {32, cuuint64_t{1} << 31};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {32, 16};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 template <int CODEC>
 KernelFn pick(int delta) {
@@ -167,11 +179,15 @@ KernelFn pick(int delta) {
   return nullptr;
 }
 
+constexpr uint32_t kCounterSlots = 1024;
+
 struct DeviceInfo {
   bool init = false;
   bool ok = false;
   int sms = 0;
   int occ[2][5] = {};
+  uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
+  uint32_t next_slot = 0;
 };
 
 DeviceInfo g_dev[64];
@@ -188,7 +204,8 @@ int device_of(const void* p) {
   return a.device;
 }
 
-int prepare(int dev, int codec, int delta, KernelFn fn, int* grid_per_sm, int* sms) {
+int prepare(int dev, int codec, int delta, KernelFn fn, int* grid_per_sm, int* sms,
+            uint32_t** counter) {
   if (dev < 0 || dev >= 64) return IZG_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lk(g_dev_mu);
   DeviceInfo& d = g_dev[dev];
@@ -198,6 +215,10 @@ int prepare(int dev, int codec, int delta, KernelFn fn, int* grid_per_sm, int* s
     if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return IZG_ERR_CUDA;
     d.ok = p.major == 10;  // sm_100 family only: no fallback path exists
     d.sms = p.multiProcessorCount;
+    if (d.ok && cudaMalloc(&d.counters, kCounterSlots * sizeof(uint32_t)) != cudaSuccess) {
+      d.ok = false;
+      return IZG_ERR_CUDA;
+    }
   }
   if (!d.ok) return IZG_ERR_NO_DEVICE;
   if (!d.occ[codec][delta]) {
@@ -205,7 +226,7 @@ int prepare(int dev, int codec, int delta, KernelFn fn, int* grid_per_sm, int* s
                              (int)kSmemBytes) != cudaSuccess)
       return IZG_ERR_CUDA;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, kSmemBytes) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarps * 32, kSmemBytes) !=
             cudaSuccess ||
         occ < 1)
       return IZG_ERR_CUDA;
@@ -213,6 +234,7 @@ int prepare(int dev, int codec, int delta, KernelFn fn, int* grid_per_sm, int* s
   }
   *grid_per_sm = d.occ[codec][delta];
   *sms = d.sms;
+  *counter = d.counters + (d.next_slot++ % kCounterSlots);
   return IZG_SUCCESS;
 }
 
@@ -250,11 +272,18 @@ extern "C" int izg_decode(int codec, int delta, const uint32_t* d_words,
   KernelFn fn = codec == IZG_SIMDBP128 ? pick<IZG_SIMDBP128>(delta) : pick<IZG_SIMDFASTPFOR>(delta);
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;
-  int rc = prepare(dev, codec, delta, fn, &per_sm, &sms);
+  uint32_t* counter = nullptr;
+  int rc = prepare(dev, codec, delta, fn, &per_sm, &sms, &counter);
   if (rc != IZG_SUCCESS) return rc;
-  const uint32_t grid = std::min<uint64_t>(n_chunks, (uint64_t)per_sm * sms);
-  fn<<<grid, kThreads, kSmemBytes, static_cast<cudaStream_t>(stream)>>>(
-      d_words, d_chunks, n_chunks, d_out, d_status, d_consumed);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t want = (n_chunks + kWarps - 1) / kWarps;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
+  if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
+  CUtensorMap omap;
+  std::memset(&omap, 0, sizeof(omap));
+  const int tma_out = make_out_map(&omap, d_out) ? 1 : 0;
+  fn<<<grid, kWarps * 32, kSmemBytes, s>>>(d_words, d_chunks, n_chunks, d_out, d_status,
+                                          d_consumed, counter, omap, tma_out);
   return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
 }
 

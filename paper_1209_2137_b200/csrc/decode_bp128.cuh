@@ -1,44 +1,41 @@
-// decode_bp128.cuh — consumer side of the fused SIMD-BP128 decoder.
+// decode_bp128.cuh — one warp decodes one SIMD-BP128 chunk.
 //
-// Restates, fused into one pass over shared memory:
+// Restates, fused into a single pass out of the warp's shared-memory ring:
 //   SimdBp128Codec::decode_deltas   codec_binpack.cpp:94-119 (meta-block walk,
-//                                   width/truncation checks)
+//                                   width/truncation checks, words consumed)
 //   unpack_vertical128              bitpack.cpp:122-161, 324-328
-//   delta_decode (D1/D4)            delta.cpp:25-89
-//   decode_array's chunk body       codec.cpp:50-68 (remainder, consumption)
-//
-// One CTA iteration = 2 meta-blocks = 32 blocks of 128 integers; consumer
-// warp w takes blocks 4w..4w+3.  Every consumer thread walks the two 16-byte
-// descriptors itself (lanes 0..15 hold one group each; a 16-lane scan gives
-// the block offsets), so the 32-hop descriptor chain costs one shared-memory
-// round trip per meta-block and never touches global memory.
+//   delta_decode (D1/D4)            delta.cpp:25-89 (+ D2/DM extensions)
+// The 16-byte meta-block descriptor is read once per meta-block by all
+// lanes; lanes 0..15 each own one group width and a 16-lane scan yields the
+// block offsets, so the descriptor chain costs one shared-memory round trip
+// per 2048 integers and never a dependent global load.
 #pragma once
 #include "izg_common.cuh"
 
 namespace izg {
 
 struct MetaWalk {
-  uint32_t width;  // this lane's group width (lanes 0..15)
-  uint32_t excl;   // words from payload start of the meta-block to its block
-  uint32_t size;   // payload words of the whole meta-block (uniform)
-  int32_t err;     // first error (uniform)
+  uint32_t width;  // lane g's group width (lanes 0..15; lanes 16..31 mirror)
+  uint32_t excl;   // payload words from the end of the descriptor to block g
+  uint32_t size;   // payload words of all present blocks (uniform)
+  int32_t err;     // first error in the reference's check order (uniform)
 };
 
-// Walk one meta-block descriptor at payload word `pos` with `groups` present
-// groups (codec_binpack.cpp:98-117); checks in the reference's order.
+// One meta-block descriptor at payload word `pos` with `groups` present
+// groups (codec_binpack.cpp:104-117): for each present group in order, a
+// width byte > 32 is an error, then a payload running past `nw` words.
 template <bool ALIGNED>
-__device__ __forceinline__ MetaWalk walk_meta(const RingView& rv, uint32_t pos, uint32_t groups,
+__device__ __forceinline__ MetaWalk walk_meta(const WarpRing& r, uint32_t pos, uint32_t groups,
                                               uint32_t nw, int lane) {
-  MetaWalk m;
   uint32_t d0, d1, d2, d3;
   if (ALIGNED) {
-    const uint4 d = lds128(rv.word_addr(pos));
+    const uint4 d = lds128(r.word_addr(pos));
     d0 = d.x; d1 = d.y; d2 = d.z; d3 = d.w;
   } else {
-    d0 = lds32(rv.word_addr(pos));
-    d1 = lds32(rv.word_addr(pos + 1));
-    d2 = lds32(rv.word_addr(pos + 2));
-    d3 = lds32(rv.word_addr(pos + 3));
+    d0 = lds32(r.word_addr(pos));
+    d1 = lds32(r.word_addr(pos + 1));
+    d2 = lds32(r.word_addr(pos + 2));
+    d3 = lds32(r.word_addr(pos + 3));
   }
   const uint32_t g = lane & 15;
   const uint32_t word = g < 4 ? d0 : g < 8 ? d1 : g < 12 ? d2 : d3;
@@ -55,6 +52,7 @@ __device__ __forceinline__ MetaWalk walk_meta(const RingView& rv, uint32_t pos, 
   const bool bad_t = valid && (pos + 4 + incl > nw);
   const uint32_t mw = __ballot_sync(0xFFFFFFFFu, bad_w) & 0xFFFFu;
   const uint32_t mt = __ballot_sync(0xFFFFFFFFu, bad_t) & 0xFFFFu;
+  MetaWalk m;
   m.err = IZG_OK;
   if (mw | mt) {
     const int first = __ffs(mw | mt) - 1;
@@ -62,85 +60,102 @@ __device__ __forceinline__ MetaWalk walk_meta(const RingView& rv, uint32_t pos, 
   }
   m.width = w;
   m.excl = incl - sz;
-  m.size = __shfl_sync(0xFFFFFFFFu, incl, groups ? groups - 1 : 0);
-  if (!groups) m.size = 0;
+  m.size = __shfl_sync(0xFFFFFFFFu, incl, groups - 1);
   return m;
 }
 
-// Decode the core blocks of one chunk.  Returns an izg_status; on success
-// *pos_out = payload words consumed by the core (decode_deltas' return).
-template <int DELTA, bool ALIGNED>
-__device__ int32_t bp128_core(RingView& rv, uint64_t* full, uint64_t* empty, uint4 (*tot)[kCW],
-                              uint32_t& tbuf, uint32_t nw, uint32_t nblocks, uint32_t* out,
-                              bool out_aligned, uint4& carry, uint32_t* pos_out) {
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int q = lane >> 3, s8 = lane & 7;
-  const int bi = 4 * warp + q;       // block within the iteration
-  const int mbl = bi >> 4;           // meta-block within the iteration
-  const uint32_t gi = bi & 15;       // group within the meta-block
-  uint32_t pos = 0;
-  for (uint32_t blk0 = 0; blk0 < nblocks; blk0 += kBlocksPerIter) {
-    // --- descriptor walk: meta-blocks A and B of this iteration ---------
-    const uint32_t gA = min(16u, nblocks - blk0);
-    if (pos + 4 > nw) return IZG_E_BP_TRUNC_DESC;
-    rv.ensure(full, 4u * (pos + 4));
-    const MetaWalk A = walk_meta<ALIGNED>(rv, pos, gA, nw, lane);
-    if (A.err) return A.err;
-    const uint32_t posA = pos;
-    pos += 4 + A.size;
-    uint32_t gB = 0, posB = pos;
-    MetaWalk B;
-    B.width = 0; B.excl = 0; B.size = 0; B.err = 0;
-    if (nblocks - blk0 > 16) {
-      gB = min(16u, nblocks - blk0 - 16);
-      if (pos + 4 > nw) return IZG_E_BP_TRUNC_DESC;
-      rv.ensure(full, 4u * (pos + 4));
-      B = walk_meta<ALIGNED>(rv, pos, gB, nw, lane);
-      if (B.err) return B.err;
-      pos += 4 + B.size;
-    }
-    rv.ensure(full, 4u * pos);
-
-    // --- unpack this thread's 4 slots x 4 lanes -------------------------
-    const uint32_t width = __shfl_sync(0xFFFFFFFFu, mbl ? B.width : A.width, gi);
-    const uint32_t excl = __shfl_sync(0xFFFFFFFFu, mbl ? B.excl : A.excl, gi);
-    const bool active = mbl ? gi < gB : gi < gA;
-    uint32_t v[4][4];
-    if (active) {
-      const uint32_t bstart = (mbl ? posB : posA) + 4 + excl;  // block payload word
-      const uint32_t mask = low_mask(width);
+// Unpack one thread's 4 slots x 4 lanes of a block whose payload starts at
+// unmasked ring byte `bb`, sliding a two-row window (lo, hi) down the block:
+// a 16-byte row is fetched only when the bit cursor enters it, so each lane
+// reads each row it needs once (bitpack.cpp:122-143 restated per lane).
+__device__ __forceinline__ void unpack_slots_aligned(const WarpRing& r, uint32_t bb,
+                                                     uint32_t width, uint32_t s8,
+                                                     uint32_t (&v)[4][4]) {
+  const uint32_t mask = low_mask(width);
+  uint32_t bit = 4u * s8 * width;
+  uint32_t row = bit >> 5;
+  uint32_t ra = bb + 16u * row;
+  uint4 lo = lds128(r.base + (ra & kRingMask));
+  uint4 hi = lds128(r.base + ((ra + 16u) & kRingMask));
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t bit = (4u * s8 + c) * width;
-        const uint32_t r = bit >> 5, sh = bit & 31u;
-        const uint32_t w0 = bstart + 4 * r;
-        if (ALIGNED) {
-          const uint4 lo = lds128(rv.word_addr(w0));
-          const uint4 hi = lds128(rv.word_addr(w0 + 4));
-          v[c][0] = funnel_r(lo.x, hi.x, sh) & mask;
-          v[c][1] = funnel_r(lo.y, hi.y, sh) & mask;
-          v[c][2] = funnel_r(lo.z, hi.z, sh) & mask;
-          v[c][3] = funnel_r(lo.w, hi.w, sh) & mask;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            v[c][j] = funnel_r(lds32(rv.word_addr(w0 + j)), lds32(rv.word_addr(w0 + 4 + j)), sh) &
-                      mask;
-        }
+  for (int c = 0; c < 4; ++c) {
+    if (c) {
+      bit += width;
+      if ((bit >> 5) != row) {
+        ++row;
+        ra += 16u;
+        lo = hi;
+        hi = lds128(r.base + ((ra + 16u) & kRingMask));
       }
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[c][j] = 0;
     }
+    const uint32_t sh = bit & 31u;
+    v[c][0] = funnel_r(lo.x, hi.x, sh) & mask;
+    v[c][1] = funnel_r(lo.y, hi.y, sh) & mask;
+    v[c][2] = funnel_r(lo.z, hi.z, sh) & mask;
+    v[c][3] = funnel_r(lo.w, hi.w, sh) & mask;
+  }
+}
 
-    // --- fused prefix sum + store (contains the iteration barrier) -----
-    uint32_t* o = active ? out + (size_t)(blk0 + bi) * 128 + 16 * s8 : nullptr;
-    scan_store<DELTA>(v, carry, tot[tbuf], warp, lane, o, out_aligned);
-    tbuf ^= 1;
-    rv.release_below(empty, 4u * pos, tid == 0);
+// Same for a payload that is not 16-byte aligned in the ring: word loads.
+__device__ __forceinline__ void unpack_slots_unaligned(const WarpRing& r, uint32_t bword,
+                                                       uint32_t width, uint32_t s8,
+                                                       uint32_t (&v)[4][4]) {
+  const uint32_t mask = low_mask(width);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t bit = (4u * s8 + c) * width;
+    const uint32_t w0 = bword + 4 * (bit >> 5), sh = bit & 31u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      v[c][j] = funnel_r(lds32(r.word_addr(w0 + j)), lds32(r.word_addr(w0 + 4 + j)), sh) & mask;
+  }
+}
+
+// Decode `nblocks` core blocks of the chunk streaming through `r`.
+// Returns an izg_status; on success *pos_out = payload words consumed.
+// `orow` is the chunk's first output row (32 integers) for the TMA path, or
+// -1 when the output is not 128-byte aligned (direct stores then).
+template <int DELTA, bool ALIGNED>
+__device__ int32_t bp128_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t nblocks,
+                              uint32_t* out, bool out_aligned, int64_t orow, uint4& carry,
+                              uint32_t* pos_out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t q = lane >> 3, s8 = lane & 7;
+  uint32_t pos = 0;
+  for (uint32_t mb0 = 0; mb0 < nblocks; mb0 += 16) {
+    const uint32_t groups = min(16u, nblocks - mb0);
+    if (pos + 4 > nw) return IZG_E_BP_TRUNC_DESC;
+    r.release_below(4u * pos);
+    r.ensure(4u * (pos + 4));
+    const MetaWalk m = walk_meta<ALIGNED>(r, pos, groups, nw, lane);
+    if (m.err) return m.err;
+    const uint32_t pay = pos + 4;  // first block's payload word
+#pragma unroll 1
+    for (uint32_t g0 = 0; g0 < groups; g0 += 4) {
+      const uint32_t gi = g0 + q;
+      const bool active = gi < groups;
+      uint32_t width = __shfl_sync(0xFFFFFFFFu, m.width, gi & 15);
+      const uint32_t excl = __shfl_sync(0xFFFFFFFFu, m.excl, gi & 15);
+      // Stream window of this iteration: its first block to its last.
+      const uint32_t first = __shfl_sync(0xFFFFFFFFu, m.excl, g0);
+      const uint32_t lastg = min(g0 + 3, groups - 1);
+      const uint32_t endw = __shfl_sync(0xFFFFFFFFu, m.excl + 4 * m.width, lastg);
+      r.release_below(4u * (pay + first));
+      r.ensure(4u * (pay + endw));
+      if (!active) width = 0;  // reads stay in the ring; values are zero
+      uint32_t v[4][4];
+      if (ALIGNED)
+        unpack_slots_aligned(r, r.ring_off() + 4u * (pay + excl), width, s8, v);
+      else
+        unpack_slots_unaligned(r, pay + excl, width, s8, v);
+      scan<DELTA>(v, carry, lane);
+      if (orow >= 0 && g0 + 4 <= groups) {
+        os.put(v, lane, (uint32_t)(orow + 4 * (mb0 + g0)));
+      } else if (active) {
+        store_direct(v, out + (size_t)(mb0 + gi) * 128 + 16 * s8, out_aligned);
+      }
+    }
+    pos = pay + m.size;
   }
   *pos_out = pos;
   return IZG_OK;

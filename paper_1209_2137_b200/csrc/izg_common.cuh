@@ -1,16 +1,19 @@
-// izg_common.cuh — pieces shared by the fused decode kernels:
-//   * the TMA ring that streams each chunk's compressed payload into shared
-//     memory (producer side and the consumer-side view),
-//   * the fused inverse differential coding + output stage for a warp that
-//     holds four 128-integer blocks in "slot-major" registers.
+// izg_common.cuh — pieces shared by the fused decode kernels.
 //
-// Register layout of a warp's four blocks ("mapping C"): lane
-// l = 8q + s8 owns block q (0..3) of the warp and, in that block, vertical
-// slots 4*s8 .. 4*s8+3 of all four lanes.  Slot s of lane j is integer 4s+j
-// of the block (bitpack.h:18-23), so each lane holds 16 CONSECUTIVE integers
-// v[c][j] = block[16*s8 + 4c + j] and the warp holds 512 consecutive
-// integers.  D4's four residue classes are the four vertical lanes
-// (delta.h:13-15), so every prefix sum is a short in-thread scan plus one
+// Execution model: one WARP decodes one chunk at a time and
+// owns a private shared-memory ring that its lane 0 fills with TMA bulk
+// copies (cp.async.bulk global->shared, completion on an mbarrier).  No
+// inter-warp synchronisation exists on the hot path: the prefix-sum carry
+// lives in the warp's registers, so tens of independent chunks are in
+// flight per SM and the per-chunk dependency chains overlap.
+//
+// Register layout of one warp iteration ("mapping C"): lane
+// l = 8q + s8 owns block q (0..3) of the iteration and, in that block,
+// vertical slots 4*s8 .. 4*s8+3 of all four lanes.  Slot s of lane j is
+// integer 4s+j of the block (bitpack.h:18-23), so every lane holds 16
+// CONSECUTIVE integers v[c][j] = block[16*s8 + 4c + j] and the warp holds 512
+// consecutive integers.  D4's four residue classes are the four vertical
+// lanes (delta.h:13-15): each prefix sum is a 3-add in-thread scan plus one
 // warp scan of per-lane totals.
 #pragma once
 #include <cstdint>
@@ -20,99 +23,94 @@
 
 namespace izg {
 
-constexpr uint32_t kStage = 4096;                // bytes per ring stage
-constexpr uint32_t kNStage = 16;                 // stages per ring
-constexpr uint32_t kRing = kStage * kNStage;     // 64 KiB
-constexpr uint32_t kRingMask = kRing - 1;
-constexpr int kCW = 8;                           // consumer warps per CTA
-constexpr int kConsumers = kCW * 32;
-constexpr int kThreads = kConsumers + 32;        // + one producer warp
-constexpr int kBlocksPerIter = kCW * 4;          // 32 blocks = 2 meta-blocks
+constexpr int kWarps = 6;                     // warps per CTA
+constexpr uint32_t kSB = 2048;                // bytes per ring stage
+constexpr uint32_t kNS = 4;                   // stages per warp ring
+constexpr uint32_t kRingBytes = kSB * kNS;    // 8 KiB per warp
+constexpr uint32_t kRingMask = kRingBytes - 1;
+constexpr uint32_t kStageOut = 2048;          // one warp iteration of output (512 ints)
+// Shared memory per CTA: kWarps rings, then 2 output staging tiles per warp
+// (1024-byte aligned for the 128-byte TMA swizzle), then the ring barriers.
+constexpr uint32_t kOutOff = kWarps * kRingBytes;
+constexpr uint32_t kBarOff = kOutOff + kWarps * 2 * kStageOut;
+constexpr size_t kSmemBytes = kBarOff + kWarps * kNS * 8;
 
-// Geometry of a chunk's payload as streamed through the ring: the 16-byte
-// aligned span [a16, a16 + total) covering the payload, `phase` = byte offset
-// of payload word 0 inside that span.  Every chunk starts on a fresh stage.
-struct StreamGeom {
-  const uint8_t* a16;
-  uint32_t total;
-  uint32_t phase;
-  uint32_t nst;
-};
+// A warp's private TMA ring.  All lanes keep identical counters; lane 0
+// issues the copies.  Chunk payloads stream as the 16-byte-aligned span
+// covering them; `phase` is payload word 0's byte offset in that span.
+struct WarpRing {
+  uint32_t base;        // shared address of the ring
+  uint8_t* gen;         // generic pointer to the ring (bulk-copy target)
+  uint64_t* full;       // kNS mbarriers
+  uint32_t g;           // stages consumed before the current chunk
+  const uint8_t* a16;   // current chunk span
+  uint32_t total, phase, nst;
+  uint32_t issued, waited, released;
+  uint64_t policy;
+  bool leader;
 
-__device__ __forceinline__ StreamGeom stream_geom(const uint32_t* words, uint64_t word_off,
-                                                  uint32_t n_words) {
-  const uintptr_t a0 = reinterpret_cast<uintptr_t>(words + word_off);
-  const uintptr_t a16 = a0 & ~uintptr_t(15);
-  const uintptr_t e16 = (a0 + 4ull * n_words + 15) & ~uintptr_t(15);
-  StreamGeom g;
-  g.a16 = reinterpret_cast<const uint8_t*>(a16);
-  g.total = static_cast<uint32_t>(e16 - a16);
-  g.phase = static_cast<uint32_t>(a0 - a16);
-  g.nst = n_words ? (g.total + kStage - 1) / kStage : 0;
-  return g;
-}
-
-// Producer: stream one chunk's span into consecutive ring stages.
-__device__ __forceinline__ void produce_chunk(uint8_t* ring, uint64_t* full, uint64_t* empty,
-                                              const StreamGeom& sg, uint32_t& g,
-                                              uint64_t policy) {
-  for (uint32_t k = 0; k < sg.nst; ++k, ++g) {
-    const uint32_t slot = g % kNStage;
-    mbar_wait(&empty[slot], ((g / kNStage) & 1u) ^ 1u);
-    const uint32_t off = k * kStage;
-    const uint32_t bytes = min(kStage, sg.total - off);
-    mbar_arrive_expect_tx(&full[slot], bytes);
-    bulk_g2s(ring + slot * kStage, sg.a16 + off, bytes, &full[slot], policy);
-  }
-}
-
-// Consumer-side view of one chunk in the ring.  Every consumer thread keeps
-// an identical copy; only consumer thread 0 arrives on `empty`.
-struct RingView {
-  uint32_t ring;      // shared-memory address of the ring
-  uint32_t g0;        // global stage index of the chunk's first stage
-  uint32_t phase;     // byte offset of payload word 0 in the first stage
-  uint32_t nst;       // stages of the chunk
-  uint32_t waited;    // stages known complete
-  uint32_t released;  // stages handed back to the producer
-
-  // Shared-memory address of payload byte `o`.
   __device__ __forceinline__ uint32_t addr(uint32_t o) const {
-    return ring + (((g0 % kNStage) * kStage + phase + o) & kRingMask);
+    return base + (((g % kNS) * kSB + phase + o) & kRingMask);
   }
   __device__ __forceinline__ uint32_t word_addr(uint32_t w) const { return addr(4u * w); }
+  // Unmasked ring offset of payload byte 0 (add a byte offset, mask, add base).
+  __device__ __forceinline__ uint32_t ring_off() const { return (g % kNS) * kSB + phase; }
+
+  __device__ __forceinline__ void refill() {
+    while (issued < nst && issued < released + kNS) {
+      if (leader) {
+        const uint32_t slot = (g + issued) % kNS;
+        const uint32_t off = issued * kSB;
+        const uint32_t bytes = min(kSB, total - off);
+        mbar_arrive_expect_tx(&full[slot], bytes);
+        bulk_g2s(gen + slot * kSB, a16 + off, bytes, &full[slot], policy);
+      }
+      ++issued;
+    }
+  }
+
+  __device__ __forceinline__ void begin(const uint32_t* words, uint64_t word_off,
+                                        uint32_t n_words) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(words + word_off);
+    const uintptr_t s = a0 & ~uintptr_t(15);
+    const uintptr_t e = (a0 + 4ull * n_words + 15) & ~uintptr_t(15);
+    a16 = reinterpret_cast<const uint8_t*>(s);
+    total = static_cast<uint32_t>(e - s);
+    phase = static_cast<uint32_t>(a0 - s);
+    nst = n_words ? (total + kSB - 1) / kSB : 0;
+    issued = waited = released = 0;
+    refill();
+  }
 
   // Block until payload bytes [0, end) have landed.
-  __device__ __forceinline__ void ensure(uint64_t* full, uint32_t end) {
+  __device__ __forceinline__ void ensure(uint32_t end) {
     const uint32_t need = phase + end;
-    while (waited * kStage < need && waited < nst) {
-      const uint32_t gg = g0 + waited;
-      mbar_wait(&full[gg % kNStage], (gg / kNStage) & 1u);
+    while (waited * kSB < need && waited < issued) {
+      const uint32_t gg = g + waited;
+      mbar_wait(&full[gg % kNS], (gg / kNS) & 1u);
       ++waited;
     }
   }
 
-  // Hand back every stage that lies entirely below payload byte `o`.
-  __device__ __forceinline__ void release_below(uint64_t* empty, uint32_t o, bool leader) {
-    uint32_t upto = (phase + o) / kStage;
+  // Recycle every stage lying entirely below payload byte `o`.
+  __device__ __forceinline__ void release_below(uint32_t o) {
+    uint32_t upto = (phase + o) / kSB;
     if (upto > waited) upto = waited;
-    while (released < upto) {
-      if (leader) mbar_arrive(&empty[(g0 + released) % kNStage]);
-      ++released;
+    if (upto > released) {
+      __syncwarp();
+      fence_proxy_async_smem();  // generic reads before the async-proxy refill
+      released = upto;
+      refill();
     }
   }
 
-  // End of chunk (call after a consumer barrier): wait for and hand back
-  // every remaining stage so the producer's phases stay in step.
-  __device__ __forceinline__ void finish(uint64_t* full, uint64_t* empty, bool leader) {
-    if (leader) {
-      for (uint32_t k = released; k < nst; ++k) {
-        const uint32_t gg = g0 + k;
-        if (k >= waited) mbar_wait(&full[gg % kNStage], (gg / kNStage) & 1u);
-        mbar_arrive(&empty[gg % kNStage]);
-      }
-    }
-    waited = released = nst;
+  // End of chunk: drain copies still in flight so slots and phases stay
+  // consistent for the next chunk.
+  __device__ __forceinline__ void end() {
+    ensure(0xFFFFFFF0u - phase);
+    __syncwarp();
+    fence_proxy_async_smem();
+    g += issued;
   }
 };
 
@@ -127,10 +125,10 @@ template <int NC>
 __device__ __forceinline__ uint4 warp_incl_scan(uint4 t, int lane) {
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, t.x, d);
-    uint32_t y1 = NC > 1 ? __shfl_up_sync(0xFFFFFFFFu, t.y, d) : 0u;
-    uint32_t y2 = NC > 2 ? __shfl_up_sync(0xFFFFFFFFu, t.z, d) : 0u;
-    uint32_t y3 = NC > 3 ? __shfl_up_sync(0xFFFFFFFFu, t.w, d) : 0u;
+    const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, t.x, d);
+    const uint32_t y1 = NC > 1 ? __shfl_up_sync(0xFFFFFFFFu, t.y, d) : 0u;
+    const uint32_t y2 = NC > 2 ? __shfl_up_sync(0xFFFFFFFFu, t.z, d) : 0u;
+    const uint32_t y3 = NC > 3 ? __shfl_up_sync(0xFFFFFFFFu, t.w, d) : 0u;
     if (lane >= d) {
       t.x += y0;
       if (NC > 1) t.y += y1;
@@ -142,73 +140,64 @@ __device__ __forceinline__ uint4 warp_incl_scan(uint4 t, int lane) {
 }
 
 // Fused inverse differential coding + store for one warp iteration.
-//   v        : the thread's 16 deltas, v[c][j] = block[16*s8 + 4c + j]
-//   carry    : running state entering the iteration (identical in all
-//              consumer threads); updated to the state after the iteration
-//   tot      : shared scratch [kCW] for warp totals (double-buffered by caller)
-//   out      : &output[16*s8] of the thread's block, or nullptr if inactive
-// Contains the per-iteration consumer barrier.
-//   D4 (delta.cpp:60-75): carry.{x,y,z,w} = last value of vertical lane j.
-//   D1 (delta.cpp:25-51): carry.x = last value.
-//   D2 (ext):             carry.x / .y = last even / odd value.
-//   DM (ext):             carry.x = last value of the last 4-vector.
+//   v     : the thread's 16 deltas, v[c][j] = block[16*s8 + 4c + j]
+//   carry : running state entering the iteration (identical in all lanes),
+//           updated to the state after the iteration:
+//     D4 (delta.cpp:60-75): carry.{x,y,z,w} = last value of vertical lane j
+//     D1 (delta.cpp:25-51): carry.x = last value
+//     D2 (ext):             carry.x / .y = last even / odd value
+//     DM (ext):             carry.x = last value of the last 4-vector
+//   out   : &output[16*s8] of the thread's block, or nullptr if inactive
 template <int DELTA>
-__device__ __forceinline__ void scan_store(uint32_t (&v)[4][4], uint4& carry, uint4* tot,
-                                           int warp, int lane, uint32_t* out,
-                                           bool out_aligned) {
-  uint4 T = make_uint4(0, 0, 0, 0);
-  uint32_t q3[4] = {0, 0, 0, 0};  // DM: inclusive prefix of lane-3 deltas
-  if (DELTA == IZG_DELTA_D4) {
-#pragma unroll
-    for (int c = 1; c < 4; ++c)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) v[c][j] += v[c - 1][j];
-    T = make_uint4(v[3][0], v[3][1], v[3][2], v[3][3]);
-  } else if (DELTA == IZG_DELTA_D1) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        s += v[c][j];
-        v[c][j] = s;
-      }
-    T.x = s;
-  } else if (DELTA == IZG_DELTA_D2) {
-    uint32_t se = 0, so = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      se += v[c][0]; v[c][0] = se;
-      so += v[c][1]; v[c][1] = so;
-      se += v[c][2]; v[c][2] = se;
-      so += v[c][3]; v[c][3] = so;
-    }
-    T.x = se;
-    T.y = so;
-  } else if (DELTA == IZG_DELTA_DM) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      s += v[c][3];
-      q3[c] = s;
-    }
-    T.x = s;
-  }
-
+__device__ __forceinline__ void scan(uint32_t (&v)[4][4], uint4& carry, int lane) {
   if (DELTA != IZG_DELTA_NONE) {
+    uint4 T = make_uint4(0, 0, 0, 0);
+    uint32_t q3[4] = {0, 0, 0, 0};  // DM: inclusive prefix of lane-3 deltas
+    if (DELTA == IZG_DELTA_D4) {
+#pragma unroll
+      for (int c = 1; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[c][j] += v[c - 1][j];
+      T = make_uint4(v[3][0], v[3][1], v[3][2], v[3][3]);
+    } else if (DELTA == IZG_DELTA_D1) {
+      uint32_t s = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          s += v[c][j];
+          v[c][j] = s;
+        }
+      T.x = s;
+    } else if (DELTA == IZG_DELTA_D2) {
+      uint32_t se = 0, so = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        se += v[c][0]; v[c][0] = se;
+        so += v[c][1]; v[c][1] = so;
+        se += v[c][2]; v[c][2] = se;
+        so += v[c][3]; v[c][3] = so;
+      }
+      T.x = se;
+      T.y = so;
+    } else {  // DM
+      uint32_t s = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        s += v[c][3];
+        q3[c] = s;
+      }
+      T.x = s;
+    }
     constexpr int NC = DELTA == IZG_DELTA_D4 ? 4 : DELTA == IZG_DELTA_D2 ? 2 : 1;
     const uint4 I = warp_incl_scan<NC>(T, lane);
-    if (lane == 31) tot[warp] = I;
-    named_bar_sync(1, kConsumers);
-    uint4 P = carry, S = carry;
-#pragma unroll
-    for (int w = 0; w < kCW; ++w) {
-      const uint4 t = tot[w];
-      if (w < warp) P = u4add(P, t);
-      S = u4add(S, t);
-    }
-    carry = S;
-    const uint4 base = u4add(P, u4sub(I, T));
+    const uint4 base = u4add(carry, u4sub(I, T));
+    uint4 tot;
+    tot.x = __shfl_sync(0xFFFFFFFFu, I.x, 31);
+    tot.y = NC > 1 ? __shfl_sync(0xFFFFFFFFu, I.y, 31) : 0u;
+    tot.z = NC > 2 ? __shfl_sync(0xFFFFFFFFu, I.z, 31) : 0u;
+    tot.w = NC > 3 ? __shfl_sync(0xFFFFFFFFu, I.w, 31) : 0u;
+    carry = u4add(carry, tot);
     if (DELTA == IZG_DELTA_D4) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -232,37 +221,73 @@ __device__ __forceinline__ void scan_store(uint32_t (&v)[4][4], uint4& carry, ui
         for (int j = 0; j < 4; ++j) v[c][j] += L;
       }
     }
-  } else {
-    named_bar_sync(1, kConsumers);
-  }
-
-  if (out) {
-    if (out_aligned) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) stg128_cs(out + 4 * c, v[c][0], v[c][1], v[c][2], v[c][3]);
-    } else {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) out[4 * c + j] = v[c][j];
-    }
   }
 }
 
+// Direct global store of the thread's 16 consecutive integers.
+__device__ __forceinline__ void store_direct(const uint32_t (&v)[4][4], uint32_t* out,
+                                             bool out_aligned) {
+  if (out_aligned) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) stg128_cs(out + 4 * c, v[c][0], v[c][1], v[c][2], v[c][3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) out[4 * c + j] = v[c][j];
+  }
+}
+
+// Output path for full warp iterations: the warp's 512 consecutive integers
+// go to a 2 KiB shared tile in the 128-byte-swizzled layout (conflict-free
+// for mapping C: the 8 lanes of a quarter-warp land in 8 distinct 16-byte
+// bank groups), then one TMA tensor store writes 16 full 128-byte rows.
+// Two tiles per warp alternate; a tile is reused once its store has read it.
+struct OutStage {
+  uint32_t base;     // shared address of the warp's two tiles (1024-aligned)
+  uint32_t buf;
+  const void* tmap;  // 2-D map of the output: rows of 32 integers, box 16 rows
+  bool leader;
+
+  __device__ __forceinline__ void put(const uint32_t (&v)[4][4], int lane, uint32_t row) {
+    if (leader) bulk_wait_read<1>();
+    __syncwarp();
+    const uint32_t t = base + buf * kStageOut;
+    const uint32_t q = lane >> 3, s8 = lane & 7;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t L = 512u * q + 64u * s8 + 16u * k;
+      const uint32_t r = L >> 7, c = (L >> 4) & 7u;
+      sts128(t + (r << 7) + ((c ^ (r & 7u)) << 4), v[k][0], v[k][1], v[k][2], v[k][3]);
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (leader) {
+      tma_store_2d(tmap, t, 0, (int)row);
+      bulk_commit();
+    }
+    buf ^= 1u;
+  }
+  __device__ __forceinline__ void drain() {
+    if (leader) bulk_wait<0>();
+    __syncwarp();
+  }
+};
+
 // Variable Byte remainder (codec_basic.cpp:27-51) of a chunk, decoded by one
-// thread from the ring, continued through the prefix sum with `carry`
+// lane from the ring and continued through the prefix sum from `carry`
 // (codec.cpp:56-66).  Returns an izg_status; *rem_bytes = bytes consumed.
 template <int DELTA>
-__device__ int32_t vbyte_tail(const RingView& rv, uint32_t byte_pos, uint32_t nbytes,
+__device__ int32_t vbyte_tail(const WarpRing& r, uint32_t byte_pos, uint32_t nbytes,
                               uint32_t core, uint32_t count, uint4 carry, uint32_t* out,
                               uint32_t* rem_bytes) {
   uint32_t pos = 0;
-  uint32_t c4[4] = {carry.x, carry.y, carry.z, carry.w};
+  uint32_t c0 = carry.x, c1 = carry.y, c2 = carry.z, c3 = carry.w;
   for (uint32_t i = 0; i < count; ++i) {
     uint32_t v = 0, shift = 0;
     for (;;) {
       if (pos >= nbytes) return IZG_E_VBYTE_TRUNCATED;
-      const uint32_t b = lds8(rv.addr(byte_pos + pos));
+      const uint32_t b = lds8(r.addr(byte_pos + pos));
       ++pos;
       if (b & 0x80u) {
         if (shift == 28 && (b & 0x70u)) return IZG_E_VBYTE_OVERFLOW;
@@ -276,17 +301,17 @@ __device__ int32_t vbyte_tail(const RingView& rv, uint32_t byte_pos, uint32_t nb
     const uint32_t idx = core + i;
     uint32_t x = v;
     if (DELTA == IZG_DELTA_D4) {
-      x += c4[idx & 3];
-      c4[idx & 3] = x;
+      const uint32_t k = idx & 3;
+      x += k == 0 ? c0 : k == 1 ? c1 : k == 2 ? c2 : c3;
+      if (k == 0) c0 = x; else if (k == 1) c1 = x; else if (k == 2) c2 = x; else c3 = x;
     } else if (DELTA == IZG_DELTA_D1) {
-      x += c4[0];
-      c4[0] = x;
+      x += c0;
+      c0 = x;
     } else if (DELTA == IZG_DELTA_D2) {
-      x += c4[idx & 1];
-      c4[idx & 1] = x;
+      if (idx & 1) { x += c1; c1 = x; } else { x += c0; c0 = x; }
     } else if (DELTA == IZG_DELTA_DM) {
-      x += c4[0];  // c4[0] = x_{4k-1}
-      if ((idx & 3) == 3) c4[0] = x;
+      x += c0;  // c0 = x_{4k-1}
+      if ((idx & 3) == 3) c0 = x;
     }
     out[idx] = x;
   }
