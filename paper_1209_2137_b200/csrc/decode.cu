@@ -36,20 +36,24 @@ __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t
 // per chunk) and decodes it end to end: stream, unpack, patch, prefix sum,
 // VByte remainder, consumption check, status.
 template <int CODEC, int DELTA>
-__global__ void __launch_bounds__(kWarps * 32, 3)
+__global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32, 3)
     decode_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                   uint32_t n_chunks, uint32_t* __restrict__ out, int32_t* __restrict__ status,
                   uint32_t* __restrict__ consumed, uint32_t* __restrict__ next_chunk,
                   const __grid_constant__ CUtensorMap omap, int tma_out) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  using LY = Layout<CODEC>;
   constexpr bool kArray = DELTA != IZG_DELTA_NONE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRing r;
   r.gen = smem + warp * kRingBytes;
   r.base = smem_u32(r.gen);
-  r.full = reinterpret_cast<uint64_t*>(smem + kBarOff) + warp * kNS;
+  r.full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff) + warp * kNS;
+  uint32_t* tab = reinterpret_cast<uint32_t*>(smem + LY::kTabOff + warp * LY::kTabBytes);
+  uint8_t* tab_b = reinterpret_cast<uint8_t*>(tab + LY::kTabEntries);
+  ExcParam* prm = reinterpret_cast<ExcParam*>(tab_b + LY::kTabEntries);
   OutStage os;
-  os.base = smem_u32(smem + kOutOff + warp * 2 * kStageOut);
+  os.base = smem_u32(smem + LY::kOutOff + warp * 2 * kStageOut);
   os.buf = 0;
   os.tmap = &omap;
   os.leader = lane == 0;
@@ -71,38 +75,37 @@ __global__ void __launch_bounds__(kWarps * 32, 3)
     int32_t st = precheck(CODEC, kArray, ch.n);
     uint32_t pos = 0;
     if (st == IZG_OK) {
-      r.begin(words, ch.word_off, ch.n_words);
+      const uint32_t* p = words + ch.word_off;
       uint32_t* o = out + ch.out_off;
       const bool oal = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
       const int64_t orow = tma_out && (ch.out_off & 31) == 0 ? (int64_t)(ch.out_off >> 5) : -1;
       const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
       uint4 carry = make_uint4(0, 0, 0, 0);
       if (CODEC == IZG_SIMDBP128) {
+        r.begin(p, ch.n_words);
         if (r.phase == 0)
           st = bp128_core<DELTA, true>(r, os, ch.n_words, core / 128, o, oal, orow, carry, &pos);
         else
           st = bp128_core<DELTA, false>(r, os, ch.n_words, core / 128, o, oal, orow, carry,
                                         &pos);
+        r.end();
       } else {
-        st = fastpfor_core<DELTA>(r, os, words + ch.word_off, ch.n_words, core / 128, o, oal,
-                                  orow, carry, &pos);
+        st = fastpfor_core<DELTA>(r, os, tab, tab_b, prm, p, ch.n_words, core / 128, o, oal, orow,
+                                  carry, &pos);
       }
       if (kArray && st == IZG_OK) {
         if (core < ch.n) {
           // Variable Byte remainder (codec.cpp:56-62).
-          r.release_below(4u * pos);
-          r.ensure(4u * ch.n_words);
           uint32_t rb = 0;
           if (lane == 0)
-            st = vbyte_tail<DELTA>(r, 4u * pos, 4u * (ch.n_words - pos), core, ch.n - core,
-                                   carry, o, &rb);
+            st = vbyte_tail<DELTA>(reinterpret_cast<const uint8_t*>(p + pos),
+                                   4u * (ch.n_words - pos), core, ch.n - core, carry, o, &rb);
           st = __shfl_sync(0xFFFFFFFFu, st, 0);
           rb = __shfl_sync(0xFFFFFFFFu, rb, 0);
           if (st == IZG_OK) pos += (rb + 3) / 4;
         }
         if (st == IZG_OK && pos != ch.n_words) st = IZG_E_PAYLOAD_SIZE;  // codec.cpp:63-64
       }
-      r.end();
     }
     if (lane == 0) {
       status[c] = st;
@@ -204,8 +207,8 @@ int device_of(const void* p) {
   return a.device;
 }
 
-int prepare(int dev, int codec, int delta, KernelFn fn, int* grid_per_sm, int* sms,
-            uint32_t** counter) {
+int prepare(int dev, int codec, int delta, KernelFn fn, int threads, size_t smem,
+            int* grid_per_sm, int* sms, uint32_t** counter) {
   if (dev < 0 || dev >= 64) return IZG_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lk(g_dev_mu);
   DeviceInfo& d = g_dev[dev];
@@ -222,11 +225,11 @@ int prepare(int dev, int codec, int delta, KernelFn fn, int* grid_per_sm, int* s
   }
   if (!d.ok) return IZG_ERR_NO_DEVICE;
   if (!d.occ[codec][delta]) {
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kSmemBytes) != cudaSuccess)
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
       return IZG_ERR_CUDA;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kWarps * 32, kSmemBytes) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) !=
             cudaSuccess ||
         occ < 1)
       return IZG_ERR_CUDA;
@@ -273,16 +276,20 @@ extern "C" int izg_decode(int codec, int delta, const uint32_t* d_words,
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;
   uint32_t* counter = nullptr;
-  int rc = prepare(dev, codec, delta, fn, &per_sm, &sms, &counter);
+  const int warps = codec == IZG_SIMDBP128 ? Layout<IZG_SIMDBP128>::kWarps
+                                           : Layout<IZG_SIMDFASTPFOR>::kWarps;
+  const size_t smem = codec == IZG_SIMDBP128 ? Layout<IZG_SIMDBP128>::kSmem
+                                             : Layout<IZG_SIMDFASTPFOR>::kSmem;
+  int rc = prepare(dev, codec, delta, fn, warps * 32, smem, &per_sm, &sms, &counter);
   if (rc != IZG_SUCCESS) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const uint64_t want = (n_chunks + kWarps - 1) / kWarps;
+  const uint64_t want = (n_chunks + warps - 1) / warps;
   const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
   if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
   CUtensorMap omap;
   std::memset(&omap, 0, sizeof(omap));
   const int tma_out = make_out_map(&omap, d_out) ? 1 : 0;
-  fn<<<grid, kWarps * 32, kSmemBytes, s>>>(d_words, d_chunks, n_chunks, d_out, d_status,
+  fn<<<grid, warps * 32, smem, s>>>(d_words, d_chunks, n_chunks, d_out, d_status,
                                           d_consumed, counter, omap, tma_out);
   return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
 }

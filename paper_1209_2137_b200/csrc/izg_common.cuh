@@ -23,17 +23,25 @@
 
 namespace izg {
 
-constexpr int kWarps = 6;                     // warps per CTA
 constexpr uint32_t kSB = 2048;                // bytes per ring stage
 constexpr uint32_t kNS = 4;                   // stages per warp ring
 constexpr uint32_t kRingBytes = kSB * kNS;    // 8 KiB per warp
 constexpr uint32_t kRingMask = kRingBytes - 1;
 constexpr uint32_t kStageOut = 2048;          // one warp iteration of output (512 ints)
-// Shared memory per CTA: kWarps rings, then 2 output staging tiles per warp
-// (1024-byte aligned for the 128-byte TMA swizzle), then the ring barriers.
-constexpr uint32_t kOutOff = kWarps * kRingBytes;
-constexpr uint32_t kBarOff = kOutOff + kWarps * 2 * kStageOut;
-constexpr size_t kSmemBytes = kBarOff + kWarps * kNS * 8;
+
+// Shared memory per CTA: the warps' rings, then 2 output staging tiles per
+// warp (1024-byte aligned for the 128-byte TMA swizzle), then per-warp
+// SIMD-FastPFOR block tables, then the ring barriers.
+template <int CODEC>
+struct Layout {
+  static constexpr int kWarps = CODEC == IZG_SIMDBP128 ? 6 : 5;
+  static constexpr uint32_t kTabEntries = 512;  // blocks per page (codec_patched.cpp:52-57)
+  static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : kTabEntries * 5 + 64;
+  static constexpr uint32_t kOutOff = kWarps * kRingBytes;
+  static constexpr uint32_t kTabOff = kOutOff + kWarps * 2 * kStageOut;
+  static constexpr uint32_t kBarOff = kTabOff + kWarps * kTabBytes;
+  static constexpr size_t kSmem = kBarOff + kWarps * kNS * 8;
+};
 
 // A warp's private TMA ring.  All lanes keep identical counters; lane 0
 // issues the copies.  Chunk payloads stream as the 16-byte-aligned span
@@ -69,9 +77,8 @@ struct WarpRing {
     }
   }
 
-  __device__ __forceinline__ void begin(const uint32_t* words, uint64_t word_off,
-                                        uint32_t n_words) {
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(words + word_off);
+  __device__ __forceinline__ void begin(const uint32_t* p, uint32_t n_words) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(p);
     const uintptr_t s = a0 & ~uintptr_t(15);
     const uintptr_t e = (a0 + 4ull * n_words + 15) & ~uintptr_t(15);
     a16 = reinterpret_cast<const uint8_t*>(s);
@@ -268,26 +275,63 @@ struct OutStage {
     }
     buf ^= 1u;
   }
+  // Split form for SIMD-FastPFOR, which patches the tile in place:
+  // acquire() -> write/patch/read the tile -> commit() or abandon().
+  __device__ __forceinline__ uint32_t acquire() {
+    if (leader) bulk_wait_read<1>();
+    __syncwarp();
+    return base + buf * kStageOut;
+  }
+  __device__ __forceinline__ void commit(const uint32_t (&v)[4][4], int lane, uint32_t row) {
+    const uint32_t t = base + buf * kStageOut;
+    write(t, v, lane);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (leader) {
+      tma_store_2d(tmap, t, 0, (int)row);
+      bulk_commit();
+    }
+    buf ^= 1u;
+  }
+  __device__ __forceinline__ void abandon() { __syncwarp(); }
+
+  // Swizzled byte address of integer p (0..511) of a warp tile.
+  __device__ __forceinline__ static uint32_t swz(uint32_t t, uint32_t p) {
+    const uint32_t L = 4u * p, r = L >> 7, c = (L >> 4) & 7u;
+    return t + (r << 7) + ((c ^ (r & 7u)) << 4) + (L & 15u);
+  }
+  __device__ __forceinline__ static void write(uint32_t t, const uint32_t (&v)[4][4], int lane) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      sts128(swz(t, 16u * lane + 4u * k), v[k][0], v[k][1], v[k][2], v[k][3]);
+  }
+  __device__ __forceinline__ static void read(uint32_t t, uint32_t (&v)[4][4], int lane) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint4 x = lds128(swz(t, 16u * lane + 4u * k));
+      v[k][0] = x.x; v[k][1] = x.y; v[k][2] = x.z; v[k][3] = x.w;
+    }
+  }
   __device__ __forceinline__ void drain() {
     if (leader) bulk_wait<0>();
     __syncwarp();
   }
 };
 
-// Variable Byte remainder (codec_basic.cpp:27-51) of a chunk, decoded by one
-// lane from the ring and continued through the prefix sum from `carry`
-// (codec.cpp:56-66).  Returns an izg_status; *rem_bytes = bytes consumed.
+// Variable Byte remainder (codec_basic.cpp:27-51) of a chunk (at most 127
+// integers), decoded by one lane straight from global memory and continued
+// through the prefix sum from `carry` (codec.cpp:56-66).  Returns an
+// izg_status; *rem_bytes = bytes consumed.
 template <int DELTA>
-__device__ int32_t vbyte_tail(const WarpRing& r, uint32_t byte_pos, uint32_t nbytes,
-                              uint32_t core, uint32_t count, uint4 carry, uint32_t* out,
-                              uint32_t* rem_bytes) {
+__device__ int32_t vbyte_tail(const uint8_t* bytes, uint32_t nbytes, uint32_t core,
+                              uint32_t count, uint4 carry, uint32_t* out, uint32_t* rem_bytes) {
   uint32_t pos = 0;
   uint32_t c0 = carry.x, c1 = carry.y, c2 = carry.z, c3 = carry.w;
   for (uint32_t i = 0; i < count; ++i) {
     uint32_t v = 0, shift = 0;
     for (;;) {
       if (pos >= nbytes) return IZG_E_VBYTE_TRUNCATED;
-      const uint32_t b = lds8(r.addr(byte_pos + pos));
+      const uint32_t b = __ldg(bytes + pos);
       ++pos;
       if (b & 0x80u) {
         if (shift == 28 && (b & 0x70u)) return IZG_E_VBYTE_OVERFLOW;
