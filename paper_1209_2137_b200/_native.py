@@ -74,6 +74,8 @@ def lib() -> C.CDLL:
     L.izg_gen_arrays.restype = C.c_int
     L.izg_gen_arrays.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                  C.c_uint64, C.c_uint32, C.c_int, vp, vp]
+    L.izg_checksum_host.restype = C.c_int
+    L.izg_checksum_host.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_int, vp]
     _lib = L
     return L
 

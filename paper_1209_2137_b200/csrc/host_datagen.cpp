@@ -37,7 +37,16 @@ void uniform_into(uint64_t n, uint64_t lo, uint64_t range, Rng& rng, uint32_t*& 
     // dense: bitmap rejection (complement when more than half is requested)
     const bool invert = n > range / 2;
     const uint64_t draws = invert ? range - n : n;
-    std::vector<uint64_t> bits((range + 63) / 64, 0);
+    const uint64_t nbw = (range + 63) / 64;
+    uint64_t small[64];
+    std::vector<uint64_t> big;
+    uint64_t* bits = small;
+    if (nbw > 64) {
+      big.assign(nbw, 0);
+      bits = big.data();
+    } else {
+      std::memset(small, 0, sizeof(uint64_t) * nbw);
+    }
     for (uint64_t k = 0; k < draws;) {
       const uint64_t v = bounded(rng, range);
       uint64_t& w = bits[v >> 6];
@@ -46,9 +55,9 @@ void uniform_into(uint64_t n, uint64_t lo, uint64_t range, Rng& rng, uint32_t*& 
       w |= b;
       ++k;
     }
-    for (uint64_t wi = 0; wi < bits.size(); ++wi) {
+    for (uint64_t wi = 0; wi < nbw; ++wi) {
       uint64_t w = invert ? ~bits[wi] : bits[wi];
-      if (invert && wi == bits.size() - 1 && range % 64) w &= (uint64_t{1} << (range % 64)) - 1;
+      if (invert && wi == nbw - 1 && range % 64) w &= (uint64_t{1} << (range % 64)) - 1;
       while (w) {
         *out++ = (uint32_t)(lo + wi * 64 + (uint64_t)__builtin_ctzll(w));
         w &= w - 1;
@@ -57,19 +66,16 @@ void uniform_into(uint64_t n, uint64_t lo, uint64_t range, Rng& rng, uint32_t*& 
     return;
   }
   if (n <= 64) {
-    // sparse and small: draw with rejection against the few values so far
-    uint32_t* first = out;
-    for (uint64_t k = 0; k < n;) {
-      const uint32_t v = (uint32_t)(lo + bounded(rng, range));
-      bool dup = false;
-      for (uint32_t* p = first; p < out; ++p)
-        if (*p == v) { dup = true; break; }
-      if (dup) continue;
-      uint32_t* p = out++;
-      while (p > first && p[-1] > v) { *p = p[-1]; --p; }  // insertion sort
-      *p = v;
-      ++k;
+    // sparse and small: draw, sort, drop duplicates, top up
+    uint32_t buf[64];
+    uint32_t have = 0;
+    while (have < n) {
+      for (uint32_t k = have; k < n; ++k) buf[k] = (uint32_t)(lo + bounded(rng, range));
+      std::sort(buf, buf + n);
+      have = (uint32_t)(std::unique(buf, buf + n) - buf);
     }
+    std::memcpy(out, buf, n * 4);
+    out += n;
     return;
   }
   // sparse and large: draw, sort, deduplicate, top up until n remain
@@ -155,6 +161,33 @@ void gen_one(int model, uint32_t n, uint32_t d, uint32_t rate_ppm, Rng& rng, uin
 }
 
 }  // namespace
+
+// izg_checksum on the host over values whose first element has global index
+// base: out[0] = sum (w+1)(2i+1) mod 2^64, out[1] = xor.
+extern "C" int izg_checksum_host(const uint32_t* v, uint64_t n, uint64_t base, int threads,
+                                 uint64_t* out) {
+  threads = std::max(1, threads);
+  std::vector<uint64_t> s(threads, 0), x(threads, 0);
+  auto work = [&](int t) {
+    const uint64_t a = n * t / threads, b = n * (t + 1) / threads;
+    uint64_t ss = 0, xx = 0;
+    for (uint64_t i = a; i < b; ++i) {
+      ss += (uint64_t(v[i]) + 1) * (2 * (base + i) + 1);
+      xx ^= v[i];
+    }
+    s[t] = ss;
+    x[t] = xx;
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) pool.emplace_back(work, t);
+  for (auto& th : pool) th.join();
+  out[0] = out[1] = 0;
+  for (int t = 0; t < threads; ++t) {
+    out[0] += s[t];
+    out[1] ^= x[t];
+  }
+  return IZG_SUCCESS;
+}
 
 extern "C" int izg_gen_arrays(int model, uint32_t count, uint32_t n, uint32_t d_lo,
                               uint32_t d_hi, uint64_t seed, uint32_t rate_ppm, int threads,

@@ -35,6 +35,8 @@ void izg_encoded_free(izg_encoded* e);
 //   model 3 RAW       : n values uniform in [0, 2^d) (unsorted; rng() & mask)
 // d is drawn per array uniformly from [d_lo, d_hi] with the array's rng
 // (only when d_lo != d_hi) and stored in d_out (nullable).
+int izg_checksum_host(const uint32_t* v, uint64_t n, uint64_t base, int threads,
+                      uint64_t* out);
 int izg_gen_arrays(int model, uint32_t count, uint32_t n, uint32_t d_lo, uint32_t d_hi,
                    uint64_t seed, uint32_t rate_ppm, int threads, uint32_t* out,
                    uint32_t* d_out);

@@ -14,7 +14,8 @@ from .codec import Codec, Encoded, raise_for_status
 class DeviceBatch:
     """An Encoded batch resident in HBM plus its output and status buffers."""
 
-    def __init__(self, codec: Codec, enc: Encoded, device=None, *, raw: bool = False):
+    def __init__(self, codec: Codec, enc: Encoded, device=None, *, raw: bool = False,
+                 out=None):
         import torch
 
         self.torch = torch
@@ -26,7 +27,11 @@ class DeviceBatch:
         self.payload_words = enc.payload_words
         self.words = torch.from_numpy(enc.words.view(np.int32)).to(self.device)
         self.table = torch.from_numpy(enc.table.view(np.uint8)).to(self.device)
-        self.out = torch.empty(max(self.n_out, 1), dtype=torch.int32, device=self.device)
+        if out is not None:
+            assert out.numel() >= self.n_out and out.dtype == torch.int32
+            self.out = out
+        else:
+            self.out = torch.empty(max(self.n_out, 1), dtype=torch.int32, device=self.device)
         self.status = torch.full((max(self.n_chunks, 1),), -1, dtype=torch.int32,
                                  device=self.device)
         self.consumed = torch.zeros(max(self.n_chunks, 1), dtype=torch.int32,
