@@ -1,0 +1,113 @@
+"""The C ABI library: loads, exports every symbol include/intzip_b200.h
+declares, host-side logic behaves, and compute entry points refuse to run
+without a B200 (there is no CPU fallback)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1209_2137_b200 as P
+from paper_1209_2137_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared(header):
+    text = open(header).read()
+    return sorted(set(re.findall(r"^\s*[A-Za-z_][\w\s\*]*?\b(izg_\w+)\s*\(", text, re.M)))
+
+
+def test_exports_every_declared_symbol(native):
+    lib = C.CDLL(N.LIB_PATH)
+    names = declared(os.path.join(ROOT, "include", "intzip_b200.h"))
+    assert set(N.ABI_SYMBOLS) <= set(names)
+    host = declared(os.path.join(ROOT, "paper_1209_2137_b200", "csrc", "intzip_b200_host.h"))
+    for name in names + host:
+        assert hasattr(lib, name), name
+
+
+def test_library_targets_sm100a(native):
+    """The fatbinary carries sm_100a SASS (cuobjdump lists the ELF arch)."""
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "--list-elf", N.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_codec_registry():
+    """make_codec (codec.cpp:99-109) for the hot-path names."""
+    assert P.make_codec("simdbp128").delta == N.DELTA_D1
+    assert P.make_codec("simdbp128-s4").delta == N.DELTA_D4
+    assert P.make_codec("simdfastpfor").codec == N.SIMDFASTPFOR
+    assert P.make_codec("simdfastpfor-s4").delta == N.DELTA_D4
+    assert P.make_codec("simdbp128-d2").delta == N.DELTA_D2
+    assert P.make_codec("simdfastpfor-dm").delta == N.DELTA_DM
+    for bad in ("lz77", "", "simdbp128-s5", "bp32"):
+        with pytest.raises(ValueError):
+            P.make_codec(bad)
+    assert P.codec_names() == ["simdbp128", "simdbp128-s4", "simdfastpfor", "simdfastpfor-s4"]
+
+
+def test_status_strings_match_reference_messages():
+    assert N.status_string(0) == "ok"
+    assert N.status_string(7) == "simdbp128: width byte exceeds 32"
+    assert N.status_string(21) == "fastpfor: exception array exhausted"
+    with pytest.raises(P.CorruptError):
+        P.raise_for_status(16)
+    with pytest.raises(ValueError):
+        P.raise_for_status(64)
+
+
+@pytest.mark.parametrize("codec", [N.SIMDBP128, N.SIMDFASTPFOR])
+def test_layout_contract(codec):
+    rng = np.random.default_rng(codec)
+    sizes = rng.integers(0, 5000, size=300).astype(np.uint32)
+    offs = np.empty(len(sizes), np.uint64)
+    total = N.lib().izg_layout_chunks(codec, N.ptr(sizes), len(sizes), N.ptr(offs))
+    phase = 3 if codec == N.SIMDFASTPFOR else 0
+    assert np.all(offs % 4 == phase)
+    ends = offs + sizes
+    assert np.all(offs[1:] >= ends[:-1])  # no overlap
+    # the 16-byte-aligned span of every chunk lies inside the allocation
+    assert total % 4 == 0 and total >= ((int(ends.max()) + 3) // 4) * 4
+    assert np.all(offs - offs % 4 >= 0)
+
+
+def test_compute_entry_points_refuse_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    L = N.lib()
+    words = np.zeros(64, np.uint32)
+    table = np.zeros(1, N.CHUNK_DTYPE)
+    out = np.zeros(128, np.uint32)
+    st = np.zeros(1, np.int32)
+    rc = L.izg_decode(0, 2, N.ptr(words), N.ptr(table), 1, N.ptr(out), N.ptr(st), None, None)
+    assert rc in (N.ERR_NO_DEVICE, N.ERR_INVALID_ARGUMENT)
+    rc = L.izg_decode_host(0, 2, N.ptr(words), 64, N.ptr(table), 1, N.ptr(out), 128, N.ptr(st))
+    assert rc == N.ERR_NO_DEVICE
+    with pytest.raises(RuntimeError):
+        P.decode_array(P.make_codec("simdbp128-s4"), P.Encoded(words, table))
+
+
+def test_decode_argument_validation():
+    L = N.lib()
+    assert L.izg_decode(7, 2, None, None, 1, None, None, None, None) == N.ERR_INVALID_ARGUMENT
+    assert L.izg_decode(0, 9, None, None, 1, None, None, None, None) == N.ERR_INVALID_ARGUMENT
+    assert L.izg_decode(0, 2, None, None, 0, None, None, None, None) == N.SUCCESS
+
+
+def test_checksum_host_matches_numpy():
+    from paper_1209_2137_b200.device import host_checksum
+
+    v = np.random.default_rng(1).integers(0, 2**32, size=100003, dtype=np.uint64).astype(np.uint32)
+    out = np.zeros(2, np.uint64)
+    N.lib().izg_checksum_host(N.ptr(v), len(v), 17, 4, N.ptr(out))
+    assert (int(out[0]), int(out[1])) == host_checksum(v, 17)
