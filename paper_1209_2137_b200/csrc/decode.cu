@@ -49,9 +49,7 @@ __global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32, 3)
   r.gen = smem + warp * kRingBytes;
   r.base = smem_u32(r.gen);
   r.full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff) + warp * kNS;
-  uint32_t* tab = reinterpret_cast<uint32_t*>(smem + LY::kTabOff + warp * LY::kTabBytes);
-  uint8_t* tab_b = reinterpret_cast<uint8_t*>(tab + LY::kTabEntries);
-  ExcParam* prm = reinterpret_cast<ExcParam*>(tab_b + LY::kTabEntries);
+  FpScratch* fsc = reinterpret_cast<FpScratch*>(smem + LY::kTabOff + warp * LY::kTabBytes);
   OutStage os;
   os.base = smem_u32(smem + LY::kOutOff + warp * 2 * kStageOut);
   os.buf = 0;
@@ -90,7 +88,7 @@ __global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32, 3)
                                         &pos);
         r.end();
       } else {
-        st = fastpfor_core<DELTA>(r, os, tab, tab_b, prm, p, ch.n_words, core / 128, o, oal, orow,
+        st = fastpfor_core<DELTA>(r, os, *fsc, p, ch.n_words, core / 128, o, oal, orow,
                                   carry, &pos);
       }
       if (kArray && st == IZG_OK) {
@@ -183,6 +181,8 @@ KernelFn pick(int delta) {
 }
 
 constexpr uint32_t kCounterSlots = 1024;
+static_assert(sizeof(FpScratch) <= Layout<IZG_SIMDFASTPFOR>::kTabBytes, "FpScratch layout");
+static_assert(Layout<IZG_SIMDFASTPFOR>::kTabBytes % 16 == 0, "FpScratch alignment");
 
 struct DeviceInfo {
   bool init = false;

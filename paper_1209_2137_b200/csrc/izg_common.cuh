@@ -23,9 +23,9 @@
 
 namespace izg {
 
-constexpr uint32_t kSB = 2048;                // bytes per ring stage
+constexpr uint32_t kSB = 1024;                // bytes per ring stage
 constexpr uint32_t kNS = 4;                   // stages per warp ring
-constexpr uint32_t kRingBytes = kSB * kNS;    // 8 KiB per warp
+constexpr uint32_t kRingBytes = kSB * kNS;    // 4 KiB per warp
 constexpr uint32_t kRingMask = kRingBytes - 1;
 constexpr uint32_t kStageOut = 2048;          // one warp iteration of output (512 ints)
 
@@ -34,9 +34,9 @@ constexpr uint32_t kStageOut = 2048;          // one warp iteration of output (5
 // SIMD-FastPFOR block tables, then the ring barriers.
 template <int CODEC>
 struct Layout {
-  static constexpr int kWarps = CODEC == IZG_SIMDBP128 ? 6 : 5;
-  static constexpr uint32_t kTabEntries = 512;  // blocks per page (codec_patched.cpp:52-57)
-  static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : kTabEntries * 5 + 64;
+  static constexpr int kWarps = CODEC == IZG_SIMDBP128 ? 8 : 6;
+  // per-warp FpScratch (decode_fastpfor.cuh), 16-byte multiple
+  static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : 64 + 4096 + 2 * 33 * 4 + 8;
   static constexpr uint32_t kOutOff = kWarps * kRingBytes;
   static constexpr uint32_t kTabOff = kOutOff + kWarps * 2 * kStageOut;
   static constexpr uint32_t kBarOff = kTabOff + kWarps * kTabBytes;

@@ -10,6 +10,8 @@ CFG = {
     "raw0": ("simdbp128", "raw", 4096, 0, 0, True),
     "raw16": ("simdbp128", "raw", 4096, 16, 0, True),
     "c4": ("simdfastpfor-s4", "geometric", 2048, 32, 100000, False),
+    "c5fp": ("simdfastpfor-s4", "cluster", 8192, (20, 29), 0, False),
+    "c5bp": ("simdbp128-s4", "cluster", 8192, (20, 29), 0, False),
 }
 name, model, count, d, rate, raw = CFG[sys.argv[1]]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5

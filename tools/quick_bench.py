@@ -44,5 +44,9 @@ if __name__ == "__main__":
         if w == "d1": run("simdbp128", "cluster", 4096, 29)
         if w == "d4u": run("simdbp128-s4", "uniform", 4096, 26)
         if w == "c4": run("simdfastpfor-s4", "geometric", 2048, 32, rate=100000)
+        if w == "c4_1": run("simdfastpfor-s4", "geometric", 2048, 32, rate=10000)
+        if w == "c5fp": run("simdfastpfor-s4", "cluster", 8192, (20, 29))
+        if w == "c5bp": run("simdbp128-s4", "cluster", 8192, (20, 29))
+        if w == "fp29": run("simdfastpfor-s4", "cluster", 8192, 29)
         if w == "raw":
             for b in (0, 8, 16, 24, 32): run("simdbp128", "raw", 4096, b, raw=True)
