@@ -4,12 +4,12 @@
 // (codec_patched.cpp:292-417) fused with the prefix sum, in three phases:
 //
 //   1. byte array (codec_patched.cpp:309-336): streamed through the warp's
-//      TMA ring and walked serially by every lane in lockstep (broadcast
-//      shared loads), checking each entry in the reference's order.  Each
-//      block's entry goes to a 64-bit shared table word:
-//      {byte offset of its positions : 17, c : 8, w = maxbits - b : 6} and
-//      {index of its first exception in array w : 17, b : 6}; the per-width
-//      running counts live in lane w-1.  Positions are range-checked when the
+//      TMA ring and walked in 128-byte windows (one shuffle per entry on the
+//      serial chain; checks lane-parallel, in the reference's order).  Each
+//      block's entry goes to a 32-bit shared table word {b : 6, w : 6, c : 8}
+//      (w = maxbits - b); byte-array offsets, packed offsets and per-width
+//      cursors are running sums rebuilt four blocks at a time in phase 3
+//      (lane w-1 keeps width w's count).  Positions are checked when the
 //      patch reads them; fp_positions_bad() settles precedence on error paths.
 //   2. exception directory (codec_patched.cpp:346-379): at most 32 dependent
 //      loads from L2 (the page tail was bulk-prefetched into L2 up front);
@@ -52,52 +52,74 @@ struct ExcParam {
 // Per-warp scratch of the SIMD-FastPFOR decoder (shared memory).
 struct __align__(16) FpScratch {
   ExcParam prm[4];
-  uint2 tab[512];          // per block, see the header comment
+  uint32_t tab[512];       // per block: b | w << 6 | c << 12 (w = maxbits - b)
   uint32_t dir_base[33];   // by width w = 1..32
   uint32_t dir_n[33];
 };
 
-// Phase 1.  Serial walk of the byte array with the reference's structural
-// checks (codec_patched.cpp:313-336).  *parsed = entries that passed.
+// Phase 1.  Walk of the byte array (codec_patched.cpp:309-336) in 128-byte
+// windows: lane l holds window bytes 4l..4l+3 and the speculative entry
+// length at each of them (2, or 3 + c when maxbits > b).  The serial chain of
+// entry starts then costs one shuffle per entry; up to 32 entries of a window
+// are validated and tabulated lane-parallel, and the first failing entry (in
+// order) ends the walk with the reference's status.  *parsed = entries that
+// passed.
 __device__ int32_t fp_parse(WarpRing& r, FpScratch& sc, uint64_t L, uint32_t nblocks, int lane,
                             uint32_t* parsed) {
   const uint32_t Lc = L > 0x7FFFFFF0ull ? 0x7FFFFFF0u : (uint32_t)L;
-  uint32_t bpos = 0, k = 0, limit = 0;
-  uint32_t cnt = 0;  // lane w-1: exceptions of width w seen so far
-  int32_t st = IZG_OK;
-  for (; k < nblocks; ++k) {
-    if (bpos + 258u > limit) {  // an entry spans at most 3 + 255 bytes
-      r.release_below(bpos);
-      r.ensure(bpos + 512u);
-      limit = r.waited * kSB > r.phase ? r.waited * kSB - r.phase : 0u;
+  uint32_t s = 0;   // next entry start (byte offset in the byte array)
+  uint32_t k0 = 0;  // entries tabulated so far
+  while (k0 < nblocks) {
+    const uint32_t W = s & ~3u;
+    r.release_below(W);
+    r.ensure(W + 128);
+    const uint32_t word = lds32(r.base + ((r.ring_off() + W + 4u * lane) & kRingMask));
+    const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, word, 1);
+    uint32_t lens[2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t x = funnel_r(word, nxt, 8 * k);
+      const uint32_t b = x & 0xFFu, mb = (x >> 8) & 0xFFu, c = (x >> 16) & 0xFFu;
+      const uint32_t len = mb > b ? 3 + c : 2;
+      if (k & 1) lens[k >> 1] |= len << 16; else lens[k >> 1] = len;
     }
-    const uint32_t a = r.ring_off() + bpos;
-    const uint32_t b = lds8(r.base + (a & kRingMask));
-    const uint32_t mb = lds8(r.base + ((a + 1) & kRingMask));
-    const uint32_t c = lds8(r.base + ((a + 2) & kRingMask));
-    const bool exc = mb > b;
-    // b <= mb <= 32 covers b <= 32; with c >= 1, bpos + 3 + c <= L implies
-    // bpos + 2 < L (the specific code is sorted out on the error path)
-    const bool bad = bpos + 2 > Lc || mb > 32 || b > mb || (exc && (c == 0 || bpos + 3 + c > Lc));
-    if (bad) {
-      if (bpos + 2 > Lc) st = IZG_E_FP_TRUNC_META;
-      else if (b > 32 || mb > 32 || b > mb) st = IZG_E_FP_WIDTHS;
-      else if (bpos + 2 >= Lc) st = IZG_E_FP_TRUNC_META;
-      else if (c == 0) st = IZG_E_FP_EMPTY_EXC;
-      else st = IZG_E_FP_TRUNC_POS;
-      break;
+    // serial chain of starts inside the window (uniform)
+    uint32_t m = 0, mystart = 0;
+    const uint32_t cap = min(32u, nblocks - k0);
+    while (m < cap && s <= W + 125) {
+      const uint32_t d = s - W;
+      const uint32_t v = __shfl_sync(0xFFFFFFFFu, (d & 2) ? lens[1] : lens[0], d >> 2);
+      if ((uint32_t)lane == m) mystart = s;
+      s += (d & 1) ? v >> 16 : v & 0xFFFFu;
+      ++m;
     }
-    const uint32_t w = mb - b;
-    const uint32_t cur = __shfl_sync(0xFFFFFFFFu, cnt, (w - 1) & 31);
-    if (exc && lane == (int)w - 1) cnt += c;
-    if (lane == 0)
-      sc.tab[k] = exc ? make_uint2((bpos + 3) | (c << 17) | (w << 25), cur | (b << 17))
-                      : make_uint2(0u, b << 17);
-    bpos += exc ? 3 + c : 2;
+    // lane-parallel checks of entries k0 .. k0+m-1, in the reference's order
+    int32_t code = IZG_OK;
+    uint32_t b = 0, mb = 0, c = 0;
+    if ((uint32_t)lane < m) {
+      const uint32_t a = r.ring_off() + mystart;
+      b = lds8(r.base + (a & kRingMask));
+      mb = lds8(r.base + ((a + 1) & kRingMask));
+      c = lds8(r.base + ((a + 2) & kRingMask));
+      const bool exc = mb > b;
+      if (mystart + 2 > Lc) code = IZG_E_FP_TRUNC_META;
+      else if (b > 32 || mb > 32 || b > mb) code = IZG_E_FP_WIDTHS;
+      else if (exc && mystart + 2 >= Lc) code = IZG_E_FP_TRUNC_META;
+      else if (exc && c == 0) code = IZG_E_FP_EMPTY_EXC;
+      else if (exc && mystart + 3 + c > Lc) code = IZG_E_FP_TRUNC_POS;
+      else
+        sc.tab[k0 + lane] = exc ? b | ((mb - b) << 6) | (c << 12) : b;
+    }
+    const uint32_t badm = __ballot_sync(0xFFFFFFFFu, code != IZG_OK);
+    if (badm) {
+      const int f = __ffs(badm) - 1;
+      *parsed = k0 + f;
+      return __shfl_sync(0xFFFFFFFFu, code, f);
+    }
+    k0 += m;
   }
-  *parsed = k;
-  if (st) return st;
-  if (bpos != L) return IZG_E_FP_BA_LEN;
+  *parsed = k0;
+  if (s != L) return IZG_E_FP_BA_LEN;
   return IZG_OK;
 }
 
@@ -106,10 +128,12 @@ __device__ int32_t fp_parse(WarpRing& r, FpScratch& sc, uint64_t L, uint32_t nbl
 // every position during its byte-array walk, before any later check.
 __device__ bool fp_positions_bad(const FpScratch& sc, const uint8_t* ba, uint32_t nb, int lane) {
   bool bad = false;
+  uint32_t bp = 0;  // entry start in the byte array
   for (uint32_t k = 0; k < nb; ++k) {
-    const uint32_t e = sc.tab[k].x;
-    const uint32_t c = (e >> 17) & 0xFFu, bp = e & 0x1FFFFu;
-    for (uint32_t i = lane; i < c; i += 32) bad |= ldg_u8(ba + bp + i) >= 128u;
+    const uint32_t e = sc.tab[k], c = e >> 12;
+    if (c)
+      for (uint32_t i = lane; i < c; i += 32) bad |= ldg_u8(ba + bp + 3 + i) >= 128u;
+    bp += c ? 3 + c : 2;
   }
   return __any_sync(0xFFFFFFFFu, bad);
 }
@@ -164,31 +188,47 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
   const uint32_t q = lane >> 3, s8 = lane & 7;
   const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
   uint32_t packed = 1;  // page word of the next block's payload
+  uint32_t bpos = 0;    // byte-array offset of the next block's entry
+  uint32_t used = 0;    // lane w-1: exceptions consumed from array w
   bool bad = false;
 #pragma unroll 1
   for (uint32_t g0 = 0; g0 < nblocks; g0 += 4) {
     const uint32_t ng = min(4u, nblocks - g0);
     // Lanes 0..3 own blocks g0..g0+3: fields, running sums over the four
     // blocks (packed words, exceptions), checks, exception parameters.
-    uint32_t b = 0, c = 0, w = 0, cur = 0, bp = 0;
+    uint32_t b = 0, c = 0, w = 0;
     if ((uint32_t)lane < ng) {
-      const uint2 e = sc.tab[g0 + lane];
-      b = e.y >> 17;
-      cur = e.y & 0x1FFFFu;
-      c = (e.x >> 17) & 0xFFu;
-      w = e.x >> 25;
-      bp = e.x & 0x1FFFFu;
+      const uint32_t e = sc.tab[g0 + lane];
+      b = e & 63u;
+      w = (e >> 6) & 63u;
+      c = e >> 12;
     }
-    uint32_t pk = 4u * b, ce = c;  // inclusive scans over lanes 0..3
+    // cursor of each block in its width array: the lane-distributed running
+    // count (lane w-1) plus earlier same-width blocks of this iteration
+    uint32_t acc = 0, add = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t wc = __shfl_sync(0xFFFFFFFFu, w | c << 8, j);
+      const uint32_t wj = wc & 0xFFu, cj = wc >> 8;
+      if (j < lane && wj == w) acc += cj;
+      if (cj && wj == (uint32_t)lane + 1) add += cj;
+    }
+    const uint32_t cur = __shfl_sync(0xFFFFFFFFu, used, (w - 1) & 31) + acc;
+    used += add;
+    // inclusive scans over lanes 0..3: packed words, exceptions, entry bytes
+    uint32_t pk = 4u * b, ce = c, bl = (uint32_t)lane < ng ? (c ? 3 + c : 2) : 0u;
 #pragma unroll
     for (int d = 1; d < 4; d <<= 1) {
       const uint32_t y0 = __shfl_up_sync(0xFFFFFFFFu, pk, d, 4);
       const uint32_t y1 = __shfl_up_sync(0xFFFFFFFFu, ce, d, 4);
+      const uint32_t y2 = __shfl_up_sync(0xFFFFFFFFu, bl, d, 4);
       if ((lane & 3) >= d) {
         pk += y0;
         ce += y1;
+        bl += y2;
       }
     }
+    const uint32_t bp = bpos + bl - (c ? c : 0u);  // this block's first position byte
     const uint32_t pk_ex = pk - 4u * b, c_ex = ce - c;
     // codec_patched.cpp:387-388 then 406-407, block by block
     const bool ov = (uint32_t)lane < ng && packed + pk > A;
@@ -210,6 +250,7 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
     const uint32_t myoff = packed + __shfl_sync(0xFFFFFFFFu, pk_ex, q);
     const uint32_t first = packed;
     packed += __shfl_sync(0xFFFFFFFFu, pk, 3);
+    bpos += __shfl_sync(0xFFFFFFFFu, bl, 3);
     const uint32_t tot = __shfl_sync(0xFFFFFFFFu, ce, 3);
     uint32_t cx[4];
     cx[0] = 0;

@@ -36,7 +36,7 @@ template <int CODEC>
 struct Layout {
   static constexpr int kWarps = CODEC == IZG_SIMDBP128 ? 8 : 6;
   // per-warp FpScratch (decode_fastpfor.cuh), 16-byte multiple
-  static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : 64 + 4096 + 2 * 33 * 4 + 8;
+  static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : 64 + 2048 + 2 * 33 * 4 + 8;
   static constexpr uint32_t kOutOff = kWarps * kRingBytes;
   static constexpr uint32_t kTabOff = kOutOff + kWarps * 2 * kStageOut;
   static constexpr uint32_t kBarOff = kTabOff + kWarps * kTabBytes;
