@@ -87,7 +87,7 @@ extern "C" uint64_t izg_layout_chunks(int codec, const uint32_t* n_words, uint32
 
 namespace {
 
-constexpr int kSlots = 3;
+constexpr int kSlots = 4;
 
 struct Slot {
   cudaStream_t stream = nullptr;
@@ -136,7 +136,7 @@ bool grow(T*& p, uint64_t& cap, uint64_t need) {
 
 extern "C" void izg_release_host_scratch(void) { t_scratch.release(); }
 
-// Pipelined over pieces of the chunk table on three streams, so the
+// Pipelined over pieces of the chunk table on four streams, so the
 // host->device copy of piece k+1, the decode of piece k and the device->host
 // copy of piece k-1 overlap (separate copy engines).  Chunks must be ordered
 // by word_off and out_off (as encode_array / izg_layout_chunks produce);
@@ -170,13 +170,14 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     if (i && (c.word_off < h_chunks[i - 1].word_off || c.out_off < h_chunks[i - 1].out_off))
       ordered = false;
   }
-  // Pieces of about 32 MiB of output.
+  // Pieces of about 64 MiB of output (enough chunks per launch to fill the
+  // GPU, small enough to keep both copy engines busy).
   std::vector<uint32_t> cuts{0};
   if (ordered) {
     uint64_t acc = 0;
     for (uint32_t i = 0; i < n_chunks; ++i) {
       acc += h_chunks[i].n;
-      if (acc >= (uint64_t{8} << 20) && i + 1 < n_chunks) {
+      if (acc >= (uint64_t{16} << 20) && i + 1 < n_chunks) {
         cuts.push_back(i + 1);
         acc = 0;
       }
