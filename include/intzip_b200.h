@@ -98,7 +98,8 @@ typedef enum izg_status {
   IZG_E_FP_PACKED_SIZE = 22,   /* codec_patched.cpp:414-415 packed area size mismatch */
   /* misuse -> std::invalid_argument */
   IZG_E_COUNT_MULTIPLE = 64,   /* codec_binpack.cpp:13-14, codec_patched.cpp:53-54 count % 128 != 0 */
-  IZG_E_PAGE_TOO_LARGE = 65    /* codec_patched.cpp:55-56 page exceeds 65536 integers */
+  IZG_E_PAGE_TOO_LARGE = 65,   /* codec_patched.cpp:55-56 page exceeds 65536 integers */
+  IZG_E_DECREASING = 66        /* delta.cpp:13 delta encode: input is not nondecreasing */
 } izg_status;
 
 /* API-level return codes (not per chunk). */
@@ -151,6 +152,23 @@ int izg_decode(int codec, int delta, const uint32_t* d_words,
  * an NCCL reduction; not part of the reference. */
 int izg_checksum(const uint32_t* d_data, uint64_t n, uint64_t* d_result,
                  void* stream);
+
+/* Fused encode of a batch of chunks, one kernel launch (secondary path;
+ * encode_array's chunk body, codec.cpp:21-35, or Codec::encode_deltas when
+ * delta == IZG_DELTA_NONE).  Per chunk i, d_chunks[i] is read as
+ *   out_off = index of the chunk's first input value in d_values,
+ *   n       = values (1..65536; a multiple of 128 for IZG_DELTA_NONE),
+ *   word_off= where its payload starts in d_words, with room for
+ *             izg_encode_bound(codec, n) words,
+ * and the kernel writes d_chunks[i].n_words.  Output words are identical to
+ * the reference encoder's.  allow_wrap != 0 takes differences mod 2^32
+ * instead of rejecting a decreasing input (IZG_E_DECREASING). */
+int izg_encode(int codec, int delta, const uint32_t* d_values, izg_chunk* d_chunks,
+               uint32_t n_chunks, uint32_t* d_words, int32_t* d_status, int allow_wrap,
+               void* stream);
+
+/* Words one chunk of n values can need (exact upper bound of the format). */
+uint64_t izg_encode_bound(int codec, uint32_t n);
 
 /* ---- host entry points (synchronous, host buffers) -------------------- */
 

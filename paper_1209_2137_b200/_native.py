@@ -74,6 +74,10 @@ def lib() -> C.CDLL:
     L.izg_gen_arrays.restype = C.c_int
     L.izg_gen_arrays.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                  C.c_uint64, C.c_uint32, C.c_int, vp, vp]
+    L.izg_encode.restype = C.c_int
+    L.izg_encode.argtypes = [C.c_int, C.c_int, vp, vp, C.c_uint32, vp, vp, C.c_int, vp]
+    L.izg_encode_bound.restype = C.c_uint64
+    L.izg_encode_bound.argtypes = [C.c_int, C.c_uint32]
     L.izg_checksum_host.restype = C.c_int
     L.izg_checksum_host.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_int, vp]
     _lib = L
@@ -82,7 +86,8 @@ def lib() -> C.CDLL:
 
 # Symbols include/intzip_b200.h declares (checked by the CPU test suite).
 ABI_SYMBOLS = ("izg_status_string", "izg_parse_codec_name", "izg_layout_chunks",
-               "izg_decode", "izg_checksum", "izg_decode_host", "izg_release_host_scratch")
+               "izg_decode", "izg_checksum", "izg_decode_host", "izg_release_host_scratch",
+               "izg_encode", "izg_encode_bound")
 
 
 def ptr(a) -> int:

@@ -15,6 +15,7 @@
 #include "../../include/intzip_b200.h"
 #include "decode_bp128.cuh"
 #include "decode_fastpfor.cuh"
+#include "encode.cuh"
 #include "izg_common.cuh"
 
 namespace izg {
@@ -311,5 +312,80 @@ extern "C" int izg_checksum(const uint32_t* d_data, uint64_t n, uint64_t* d_resu
     checksum_kernel<<<grid, 256, 0, s>>>(d_data, n,
                                          reinterpret_cast<unsigned long long*>(d_result));
   }
+  return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+}
+
+// ---- encoder (secondary path) ---------------------------------------------
+
+namespace izg {
+
+using EncodeFn = void (*)(const uint32_t*, izg_chunk*, uint32_t, uint32_t*, int32_t*, uint32_t*);
+
+template <bool WRAP>
+EncodeFn pick_enc(int delta) {
+  switch (delta) {
+    case IZG_DELTA_NONE: return bp128_encode_kernel<IZG_DELTA_NONE, WRAP>;
+    case IZG_DELTA_D1: return bp128_encode_kernel<IZG_DELTA_D1, WRAP>;
+    case IZG_DELTA_D4: return bp128_encode_kernel<IZG_DELTA_D4, WRAP>;
+    case IZG_DELTA_D2: return bp128_encode_kernel<IZG_DELTA_D2, WRAP>;
+    case IZG_DELTA_DM: return bp128_encode_kernel<IZG_DELTA_DM, WRAP>;
+  }
+  return nullptr;
+}
+
+}  // namespace izg
+
+extern "C" uint64_t izg_encode_bound(int codec, uint32_t n) {
+  return izg::izg_encode_bound_impl(codec, n);
+}
+
+extern "C" int izg_encode(int codec, int delta, const uint32_t* d_values, izg_chunk* d_chunks,
+                          uint32_t n_chunks, uint32_t* d_words, int32_t* d_status, int allow_wrap,
+                          void* stream) {
+  using namespace izg;
+  if (codec != IZG_SIMDBP128) return IZG_ERR_INVALID_ARGUMENT;  // FastPFOR: host encoder
+  if (delta < IZG_DELTA_NONE || delta > IZG_DELTA_DM) return IZG_ERR_INVALID_ARGUMENT;
+  if (n_chunks == 0) return IZG_SUCCESS;
+  if (!d_values || !d_chunks || !d_words || !d_status) return IZG_ERR_INVALID_ARGUMENT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return IZG_ERR_NO_DEVICE;
+  }
+  const int dev = device_of(d_status);
+  if (dev < 0) return IZG_ERR_INVALID_ARGUMENT;
+  EncodeFn fn = allow_wrap ? pick_enc<true>(delta) : pick_enc<false>(delta);
+  DeviceGuard guard(dev);
+  int per_sm = 0, sms = 0;
+  uint32_t* counter = nullptr;
+  // occupancy slot 0 of the (unused) BP128 raw-mode table is not shared with
+  // decode kernels: encode uses static shared memory only
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DeviceInfo& d = g_dev[dev];
+    if (!d.init) {
+      d.init = true;
+      cudaDeviceProp p;
+      if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return IZG_ERR_CUDA;
+      d.ok = p.major == 10;
+      d.sms = p.multiProcessorCount;
+      if (d.ok && cudaMalloc(&d.counters, kCounterSlots * sizeof(uint32_t)) != cudaSuccess) {
+        d.ok = false;
+        return IZG_ERR_CUDA;
+      }
+    }
+    if (!d.ok) return IZG_ERR_NO_DEVICE;
+    sms = d.sms;
+    counter = d.counters + (d.next_slot++ % kCounterSlots);
+  }
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kEncWarps * 32, 0) !=
+          cudaSuccess ||
+      per_sm < 1)
+    return IZG_ERR_CUDA;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t want = (n_chunks + kEncWarps - 1) / kEncWarps;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
+  if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
+  fn<<<grid, kEncWarps * 32, 0, s>>>(d_values, d_chunks, n_chunks, d_words, d_status, counter);
   return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
 }

@@ -38,6 +38,7 @@ extern "C" const char* izg_status_string(int32_t s) {
     case IZG_E_FP_PACKED_SIZE: return "fastpfor: packed area size mismatch";
     case IZG_E_COUNT_MULTIPLE: return "count must be a multiple of 128";
     case IZG_E_PAGE_TOO_LARGE: return "patched codec: page exceeds 65536 integers";
+    case IZG_E_DECREASING: return "delta encode: input is not nondecreasing";
     default: return "unknown status";
   }
 }

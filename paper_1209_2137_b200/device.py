@@ -80,3 +80,42 @@ def host_checksum(values: np.ndarray, base_index: int = 0) -> tuple[int, int]:
         s = int(np.sum((v + np.uint64(1)) * (np.uint64(2) * i + np.uint64(1)), dtype=np.uint64))
     x = int(np.bitwise_xor.reduce(v)) if len(v) else 0
     return s, x
+
+
+def encode_on_device(codec: Codec, values, value_off, counts, *, allow_wrap: bool = False,
+                     raw: bool = False, device=None):
+    """GPU encoder (izg_encode): returns (Encoded with host copies, statuses).
+
+    Chunks are placed in slots of izg_encode_bound words (4-word aligned), so
+    the result satisfies izg_decode's placement contract as is."""
+    import torch
+
+    dev = torch.device(device or "cuda")
+    L = N.lib()
+    counts = np.ascontiguousarray(counts, dtype=np.uint32)
+    value_off = np.ascontiguousarray(value_off, dtype=np.uint64)
+    bounds = np.array([L.izg_encode_bound(codec.codec, int(n)) for n in counts], np.uint64)
+    slots = (bounds + 3) // 4 * 4
+    word_off = np.concatenate([[0], np.cumsum(slots)[:-1]]).astype(np.uint64) if len(slots) else slots
+    total = int(slots.sum()) + 4
+    table = np.zeros(len(counts), dtype=N.CHUNK_DTYPE)
+    table["word_off"] = word_off
+    table["n"] = counts
+    table["out_off"] = value_off
+    vals = values if isinstance(values, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(values, dtype=np.uint32).view(np.int32))
+    vals = vals.to(dev)
+    d_table = torch.from_numpy(table.view(np.uint8)).to(dev)
+    d_words = torch.zeros(total, dtype=torch.int32, device=dev)
+    d_status = torch.full((max(len(counts), 1),), -1, dtype=torch.int32, device=dev)
+    delta = N.DELTA_NONE if raw else codec.delta
+    s = torch.cuda.current_stream(dev)
+    rc = L.izg_encode(codec.codec, delta, N.ptr(vals), N.ptr(d_table), len(counts),
+                      N.ptr(d_words), N.ptr(d_status), int(allow_wrap), s.cuda_stream)
+    if rc != N.SUCCESS:
+        raise RuntimeError(f"izg_encode failed: {rc}")
+    out_table = d_table.cpu().numpy().view(N.CHUNK_DTYPE).copy()
+    # as a decode batch the outputs go back to back
+    out_table["out_off"] = value_off
+    enc = Encoded(d_words.cpu().numpy().view(np.uint32), out_table)
+    return enc, d_status[:len(counts)].cpu().numpy()
