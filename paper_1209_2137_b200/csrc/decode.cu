@@ -322,13 +322,23 @@ namespace izg {
 using EncodeFn = void (*)(const uint32_t*, izg_chunk*, uint32_t, uint32_t*, int32_t*, uint32_t*);
 
 template <bool WRAP>
-EncodeFn pick_enc(int delta) {
-  switch (delta) {
-    case IZG_DELTA_NONE: return bp128_encode_kernel<IZG_DELTA_NONE, WRAP>;
-    case IZG_DELTA_D1: return bp128_encode_kernel<IZG_DELTA_D1, WRAP>;
-    case IZG_DELTA_D4: return bp128_encode_kernel<IZG_DELTA_D4, WRAP>;
-    case IZG_DELTA_D2: return bp128_encode_kernel<IZG_DELTA_D2, WRAP>;
-    case IZG_DELTA_DM: return bp128_encode_kernel<IZG_DELTA_DM, WRAP>;
+EncodeFn pick_enc(int codec, int delta) {
+  if (codec == IZG_SIMDBP128) {
+    switch (delta) {
+      case IZG_DELTA_NONE: return bp128_encode_kernel<IZG_DELTA_NONE, WRAP>;
+      case IZG_DELTA_D1: return bp128_encode_kernel<IZG_DELTA_D1, WRAP>;
+      case IZG_DELTA_D4: return bp128_encode_kernel<IZG_DELTA_D4, WRAP>;
+      case IZG_DELTA_D2: return bp128_encode_kernel<IZG_DELTA_D2, WRAP>;
+      case IZG_DELTA_DM: return bp128_encode_kernel<IZG_DELTA_DM, WRAP>;
+    }
+  } else {
+    switch (delta) {
+      case IZG_DELTA_NONE: return fastpfor_encode_kernel<IZG_DELTA_NONE, WRAP>;
+      case IZG_DELTA_D1: return fastpfor_encode_kernel<IZG_DELTA_D1, WRAP>;
+      case IZG_DELTA_D4: return fastpfor_encode_kernel<IZG_DELTA_D4, WRAP>;
+      case IZG_DELTA_D2: return fastpfor_encode_kernel<IZG_DELTA_D2, WRAP>;
+      case IZG_DELTA_DM: return fastpfor_encode_kernel<IZG_DELTA_DM, WRAP>;
+    }
   }
   return nullptr;
 }
@@ -343,7 +353,7 @@ extern "C" int izg_encode(int codec, int delta, const uint32_t* d_values, izg_ch
                           uint32_t n_chunks, uint32_t* d_words, int32_t* d_status, int allow_wrap,
                           void* stream) {
   using namespace izg;
-  if (codec != IZG_SIMDBP128) return IZG_ERR_INVALID_ARGUMENT;  // FastPFOR: host encoder
+  if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return IZG_ERR_INVALID_ARGUMENT;
   if (delta < IZG_DELTA_NONE || delta > IZG_DELTA_DM) return IZG_ERR_INVALID_ARGUMENT;
   if (n_chunks == 0) return IZG_SUCCESS;
   if (!d_values || !d_chunks || !d_words || !d_status) return IZG_ERR_INVALID_ARGUMENT;
@@ -354,7 +364,8 @@ extern "C" int izg_encode(int codec, int delta, const uint32_t* d_values, izg_ch
   }
   const int dev = device_of(d_status);
   if (dev < 0) return IZG_ERR_INVALID_ARGUMENT;
-  EncodeFn fn = allow_wrap ? pick_enc<true>(delta) : pick_enc<false>(delta);
+  EncodeFn fn = allow_wrap ? pick_enc<true>(codec, delta) : pick_enc<false>(codec, delta);
+  const size_t esmem = codec == IZG_SIMDBP128 ? 0 : kEncWarps * sizeof(FpEncScratch);
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;
   uint32_t* counter = nullptr;
@@ -378,7 +389,10 @@ extern "C" int izg_encode(int codec, int delta, const uint32_t* d_values, izg_ch
     sms = d.sms;
     counter = d.counters + (d.next_slot++ % kCounterSlots);
   }
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kEncWarps * 32, 0) !=
+  if (esmem && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)esmem) != cudaSuccess)
+    return IZG_ERR_CUDA;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kEncWarps * 32, esmem) !=
           cudaSuccess ||
       per_sm < 1)
     return IZG_ERR_CUDA;
@@ -386,6 +400,6 @@ extern "C" int izg_encode(int codec, int delta, const uint32_t* d_values, izg_ch
   const uint64_t want = (n_chunks + kEncWarps - 1) / kEncWarps;
   const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
   if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
-  fn<<<grid, kEncWarps * 32, 0, s>>>(d_values, d_chunks, n_chunks, d_words, d_status, counter);
+  fn<<<grid, kEncWarps * 32, esmem, s>>>(d_values, d_chunks, n_chunks, d_words, d_status, counter);
   return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
 }

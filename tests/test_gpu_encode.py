@@ -12,6 +12,7 @@ from tests.helpers import assorted_arrays, chunks_of, random_sorted
 pytestmark = pytest.mark.gpu
 
 BP_NAMES = ["simdbp128", "simdbp128-s4", "simdbp128-d2", "simdbp128-dm"]
+FP_NAMES = ["simdfastpfor", "simdfastpfor-s4", "simdfastpfor-d2", "simdfastpfor-dm"]
 
 
 def _chunks(arr):
@@ -20,7 +21,7 @@ def _chunks(arr):
     return offs, counts
 
 
-@pytest.mark.parametrize("name", BP_NAMES)
+@pytest.mark.parametrize("name", BP_NAMES + FP_NAMES)
 def test_gpu_encode_matches_host_encoder(cuda, name):
     codec = P.make_codec(name)
     for arr in assorted_arrays(seed=zlib.crc32(name.encode()) % 101):
@@ -33,7 +34,7 @@ def test_gpu_encode_matches_host_encoder(cuda, name):
         assert np.array_equal(P.decode_array(codec, genc), arr)
 
 
-@pytest.mark.parametrize("name", ["simdbp128", "simdbp128-s4"])
+@pytest.mark.parametrize("name", ["simdbp128", "simdbp128-s4", "simdfastpfor", "simdfastpfor-s4"])
 def test_gpu_encode_matches_reference(cuda, ref, name):
     codec = P.make_codec(name)
     rng = np.random.default_rng(8)
@@ -47,24 +48,29 @@ def test_gpu_encode_matches_reference(cuda, ref, name):
             assert n1 == n2 and np.array_equal(a, b)
 
 
-def test_gpu_encode_raw_every_width(cuda, ref):
-    codec = P.make_codec("simdbp128")
+@pytest.mark.parametrize("codec_name", ["simdbp128", "simdfastpfor"])
+def test_gpu_encode_raw_every_width(cuda, ref, codec_name):
+    codec = P.make_codec(codec_name)
     rng = np.random.default_rng(9)
     vals, counts = [], []
     for b in range(33):
         n = 128 * (1 + b % 20)
-        vals.append((rng.integers(0, 2**32, size=n, dtype=np.uint64) & ((1 << b) - 1)).astype(np.uint32))
+        v = (rng.integers(0, 2**32, size=n, dtype=np.uint64) & ((1 << b) - 1)).astype(np.uint32)
+        if b % 3 == 0:  # outliers: FastPFOR exceptions of many widths
+            v[::29] = rng.integers(0, 2**32, size=len(v[::29]), dtype=np.uint64)
+        vals.append(v)
         counts.append(n)
     flat = np.concatenate(vals)
     offs = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
     genc, st = encode_on_device(codec, flat, offs, counts, raw=True)
     assert np.all(st == 0)
     for (n, w), v in zip(chunks_of(genc), vals):
-        assert np.array_equal(w, ref.encode_deltas("simdbp128", v))
+        assert np.array_equal(w, ref.encode_deltas(codec_name, v))
 
 
-def test_gpu_encode_wrap_and_decreasing(cuda, ref):
-    codec = P.make_codec("simdbp128-s4")
+@pytest.mark.parametrize("name", ["simdbp128-s4", "simdfastpfor-s4"])
+def test_gpu_encode_wrap_and_decreasing(cuda, ref, name):
+    codec = P.make_codec(name)
     vals, _ = P.gen_arrays("geometric", 3, 65536, 32, seed=4, rate_ppm=50000)
     flat = vals.reshape(-1)
     offs, counts = np.arange(3, dtype=np.uint64) * 65536, np.full(3, 65536, np.uint32)
@@ -73,15 +79,16 @@ def test_gpu_encode_wrap_and_decreasing(cuda, ref):
     genc, st = encode_on_device(codec, flat, offs, counts, allow_wrap=True)
     assert np.all(st == 0)
     for i, (n, w) in enumerate(chunks_of(genc)):
-        assert np.array_equal(w, ref.encode_chunk_wrapping("simdbp128-s4", vals[i]))
+        assert np.array_equal(w, ref.encode_chunk_wrapping(name, vals[i]))
     bad = np.array([5, 3] + list(range(10, 300)), np.uint32)
     _, st = encode_on_device(P.make_codec("simdbp128"), bad, np.array([0], np.uint64),
                              np.array([len(bad)], np.uint32))
     assert st[0] == 66
 
 
-def test_gpu_encode_large_batch_roundtrip(cuda):
-    codec = P.make_codec("simdbp128-s4")
+@pytest.mark.parametrize("name", ["simdbp128-s4", "simdfastpfor-s4"])
+def test_gpu_encode_large_batch_roundtrip(cuda, name):
+    codec = P.make_codec(name)
     vals, _ = P.gen_arrays("cluster", 512, 65536, (20, 29), seed=77)
     flat = vals.reshape(-1)
     offs, counts = np.arange(512, dtype=np.uint64) * 65536, np.full(512, 65536, np.uint32)
