@@ -50,3 +50,43 @@ if __name__ == "__main__":
         if w == "fp29": run("simdfastpfor-s4", "cluster", 8192, 29)
         if w == "raw":
             for b in (0, 8, 16, 24, 32): run("simdbp128", "raw", 4096, b, raw=True)
+
+
+def run_encode(name, model, count, d, rate=0, reps=10):
+    """GPU encoder throughput (izg_encode) on device-resident values."""
+    import paper_1209_2137_b200._native as N
+    codec = P.make_codec(name)
+    vals, _ = P.gen_arrays(model, count, 65536, d, seed=3, rate_ppm=rate)
+    flat = vals.reshape(-1)
+    L = N.lib()
+    counts = np.full(count, 65536, np.uint32)
+    bound = (L.izg_encode_bound(codec.codec, 65536) + 3) // 4 * 4
+    table = np.zeros(count, dtype=N.CHUNK_DTYPE)
+    table["word_off"] = np.arange(count, dtype=np.uint64) * bound
+    table["n"] = counts
+    table["out_off"] = np.arange(count, dtype=np.uint64) * 65536
+    dv = torch.from_numpy(flat.view(np.int32)).cuda()
+    dt = torch.from_numpy(table.view(np.uint8)).cuda()
+    dw = torch.zeros(count * bound + 4, dtype=torch.int32, device="cuda")
+    ds = torch.zeros(count, dtype=torch.int32, device="cuda")
+    wrap = int(model == "geometric")
+    def go():
+        rc = L.izg_encode(codec.codec, codec.delta, dv.data_ptr(), dt.data_ptr(), count, dw.data_ptr(),
+                          ds.data_ptr(), wrap, torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+    for _ in range(3): go()
+    torch.cuda.synchronize()
+    assert int(ds.abs().sum()) == 0
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(); go(); e1.record(); torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    t = float(np.median(ts))
+    print(json.dumps(dict(encode=name, model=model, gints=round(flat.size / t / 1e9, 2), ms=round(t * 1e3, 3))), flush=True)
+
+
+if __name__ == "__main__" and "enc" in sys.argv[1:]:
+    run_encode("simdbp128-s4", "cluster", 4096, (20, 29))
+    run_encode("simdfastpfor-s4", "cluster", 4096, (20, 29))
+    run_encode("simdfastpfor-s4", "geometric", 2048, 32, rate=100000)
