@@ -104,8 +104,17 @@ struct Slot {
 struct Scratch {
   int device = -1;
   Slot slot[kSlots];
-  std::vector<int32_t> status_host;
+  // pinned staging for the chunk table and the statuses, so every copy of
+  // the pipeline is truly asynchronous (pageable copies block the host)
+  izg_chunk* pin_table = nullptr;
+  int32_t* pin_status = nullptr;
+  uint64_t pin_cap = 0;
   void release() {
+    if (pin_table) cudaFreeHost(pin_table);
+    if (pin_status) cudaFreeHost(pin_status);
+    pin_table = nullptr;
+    pin_status = nullptr;
+    pin_cap = 0;
     for (auto& s : slot) {
       if (s.words) cudaFree(s.words);
       if (s.table) cudaFree(s.table);
@@ -185,8 +194,21 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     }
   }
   cuts.push_back(n_chunks);
-  S.status_host.assign(h_status ? 0 : n_chunks, 0);
-  int32_t* st_host = h_status ? h_status : S.status_host.data();
+  if (S.pin_cap < n_chunks) {
+    if (S.pin_table) cudaFreeHost(S.pin_table);
+    if (S.pin_status) cudaFreeHost(S.pin_status);
+    S.pin_table = nullptr;
+    S.pin_status = nullptr;
+    S.pin_cap = 0;
+    if (cudaHostAlloc(&S.pin_table, sizeof(izg_chunk) * n_chunks, cudaHostAllocDefault) !=
+            cudaSuccess ||
+        cudaHostAlloc(&S.pin_status, sizeof(int32_t) * n_chunks, cudaHostAllocDefault) !=
+            cudaSuccess)
+      return IZG_ERR_CUDA;
+    S.pin_cap = n_chunks;
+  }
+  std::memcpy(S.pin_table, h_chunks, sizeof(izg_chunk) * n_chunks);
+  int32_t* st_host = S.pin_status;
   int rc = IZG_SUCCESS;
   for (size_t p = 0; p + 1 < cuts.size() && rc == IZG_SUCCESS; ++p) {
     Slot& s = S.slot[p % kSlots];
@@ -220,7 +242,7 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     }
     cudaMemsetAsync(s.words + wcopy, 0, (wneed - wcopy) * 4, s.stream);
     cudaMemcpyAsync(s.words, h_words + wlo, wcopy * 4, cudaMemcpyHostToDevice, s.stream);
-    cudaMemcpyAsync(s.table, h_chunks + c0, sizeof(izg_chunk) * nc, cudaMemcpyHostToDevice,
+    cudaMemcpyAsync(s.table, S.pin_table + c0, sizeof(izg_chunk) * nc, cudaMemcpyHostToDevice,
                     s.stream);
     // Shifted base pointers: the kernel adds the table's absolute offsets.
     const int r = izg_decode(codec, delta, s.words - wlo, s.table, nc, s.out - olo, s.status,
@@ -236,6 +258,7 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
   for (auto& s : S.slot)
     if (cudaStreamSynchronize(s.stream) != cudaSuccess) rc = IZG_ERR_CUDA;
   if (rc != IZG_SUCCESS) return rc;
+  if (h_status) std::memcpy(h_status, st_host, sizeof(int32_t) * n_chunks);
   for (uint32_t i = 0; i < n_chunks; ++i)
     if (st_host[i] != IZG_OK) return IZG_ERR_CORRUPT;
   return IZG_SUCCESS;
