@@ -37,7 +37,7 @@ __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t
 // per chunk) and decodes it end to end: stream, unpack, patch, prefix sum,
 // VByte remainder, consumption check, status.
 template <int CODEC, int DELTA>
-__global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32, 3)
+__global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32) __maxnreg__(Layout<CODEC>::kMaxRegs)
     decode_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                   uint32_t n_chunks, uint32_t* __restrict__ out, int32_t* __restrict__ status,
                   uint32_t* __restrict__ consumed, uint32_t* __restrict__ next_chunk,

@@ -35,6 +35,8 @@ constexpr uint32_t kStageOut = 2048;          // one warp iteration of output (5
 template <int CODEC>
 struct Layout {
   static constexpr int kWarps = CODEC == IZG_SIMDBP128 ? 8 : 6;
+  // registers per thread so that 3 CTAs fit in the 64K-register file
+  static constexpr int kMaxRegs = CODEC == IZG_SIMDBP128 ? 80 : 96;
   // per-warp FpScratch (decode_fastpfor.cuh), 16-byte multiple
   static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : 64 + 2048 + 2 * 33 * 4 + 8;
   static constexpr uint32_t kOutOff = kWarps * kRingBytes;
