@@ -40,18 +40,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
                  : "memory");
 }
 
-// Per-block exception parameters of one warp iteration, in shared memory so
-// a lane finds its exception's block with one broadcast load.
-struct ExcParam {
-  int32_t pbase;  // byte-array offset of exception e is pbase + e
-  int32_t rbase;  // index in its width array is rbase + e
-  uint32_t base;  // page word of that array
-  uint32_t wb;    // w | b << 8
-};
-
 // Per-warp scratch of the SIMD-FastPFOR decoder (shared memory).
 struct __align__(16) FpScratch {
-  ExcParam prm[4];
   uint32_t tab[512];       // per block: b | w << 6 | c << 12 (w = maxbits - b)
   uint32_t dir_base[33];   // by width w = 1..32
   uint32_t dir_n[33];
@@ -229,7 +219,7 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
       }
     }
     const uint32_t bp = bpos + bl - (c ? c : 0u);  // this block's first position byte
-    const uint32_t pk_ex = pk - 4u * b, c_ex = ce - c;
+    const uint32_t pk_ex = pk - 4u * b;
     // codec_patched.cpp:387-388 then 406-407, block by block
     const bool ov = (uint32_t)lane < ng && packed + pk > A;
     const bool ex = c && cur + c > sc.dir_n[w];
@@ -238,25 +228,21 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
       const int k = __ffs(em) - 1;
       return (__ballot_sync(0xFFFFFFFFu, ov) >> k) & 1u ? IZG_E_FP_OVERRUN : IZG_E_FP_EXHAUSTED;
     }
-    if (c) {
-      ExcParam x;
-      x.pbase = (int32_t)bp - (int32_t)c_ex;
-      x.rbase = (int32_t)cur - (int32_t)c_ex;
-      x.base = sc.dir_base[w];
-      x.wb = w | b << 8;
-      sc.prm[lane] = x;
-    }
+    // per-lane view of its own block q (lanes 8q..8q+7 patch block q)
     const uint32_t myb = __shfl_sync(0xFFFFFFFFu, b, q);
     const uint32_t myoff = packed + __shfl_sync(0xFFFFFFFFu, pk_ex, q);
+    const uint32_t myc = __shfl_sync(0xFFFFFFFFu, c, q);
+    const uint32_t myw = __shfl_sync(0xFFFFFFFFu, w, q);
+    const uint32_t mybp = __shfl_sync(0xFFFFFFFFu, bp, q);
+    const uint32_t mycur = __shfl_sync(0xFFFFFFFFu, cur, q);
+    const uint32_t mybase = sc.dir_base[myw];
     const uint32_t first = packed;
     packed += __shfl_sync(0xFFFFFFFFu, pk, 3);
     bpos += __shfl_sync(0xFFFFFFFFu, bl, 3);
     const uint32_t tot = __shfl_sync(0xFFFFFFFFu, ce, 3);
-    uint32_t cx[4];
-    cx[0] = 0;
-    cx[1] = __shfl_sync(0xFFFFFFFFu, ce, 0);
-    cx[2] = __shfl_sync(0xFFFFFFFFu, ce, 1);
-    cx[3] = __shfl_sync(0xFFFFFFFFu, ce, 2);
+    // rounds of 8 exceptions per block: the longest list of the four
+    uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));
+    mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));
 
     // Stream window: packed words [first, packed) (the stream starts at word 1).
     r.release_below(4u * (first - 1));
@@ -267,46 +253,37 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
       unpack_slots_aligned(r, r.ring_off() + 4u * (myoff - 1), myb, s8, v);
     else
       unpack_slots_unaligned(r, myoff - 1, myb, s8, v);
-    __syncwarp();  // prm visible to every lane
-
     if (tot) {
       // Patch through the warp's output tile (swizzled; see OutStage).
       const uint32_t t = os.acquire();
       OutStage::write(t, v, lane);
       __syncwarp();
-      // 32 exceptions per round, up to 4 rounds per batch: a batch issues all
-      // its loads before its first shared-memory OR.
-      const uint32_t nr = (tot + 31) >> 5;
-      for (uint32_t r0 = 0; r0 < nr; r0 += 4) {
-        // (a) issue every load of the batch; nothing consumes them yet
-        uint32_t pp[4], lo[4], hi[4], sh[4], ek[4];
+      // Lanes 8q..8q+7 patch block q, eight exceptions per round; two
+      // rounds per batch issue all their loads before the first OR.
+      const uint32_t wmask = low_mask(myw), w4 = 4u * myw;
+      for (uint32_t e0 = s8; e0 < mxc; e0 += 16) {
+        uint32_t pp[2], lo[2], hi[2], sh[2];
+        bool ok[2];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (r0 + j < nr) {
-            const uint32_t e0 = 32u * (r0 + j) + lane;
-            const uint32_t e = e0 < tot ? e0 : tot - 1;
-            const uint32_t k = (e >= cx[1]) + (e >= cx[2]) + (e >= cx[3]);
-            const ExcParam x = sc.prm[k];
-            const uint32_t w = x.wb & 0xFFu;
-            const uint32_t rr = (uint32_t)(x.rbase + (int32_t)e);
-            const uint32_t tt = rr & 127u, bit = (tt >> 2) * w;
-            const uint32_t word = x.base + (rr >> 7) * 4u * w + 4u * (bit >> 5) + (tt & 3u);
-            sh[j] = bit & 31u;
-            pp[j] = ldg_u8(ba + (x.pbase + (int32_t)e));
-            lo[j] = ldg_u32(page + word);
-            hi[j] = ldg_u32(page + word + (sh[j] + w > 32 ? 4u : 0u));
-            ek[j] = k | (x.wb << 8);  // k | w << 8 | b << 16
-          }
+        for (int j = 0; j < 2; ++j) {
+          const uint32_t e = e0 + 8u * j;
+          ok[j] = e < myc;
+          const uint32_t ee = ok[j] ? e : 0u;  // myc == 0: loads stay in the page
+          const uint32_t rr = mycur + ee;
+          const uint32_t tt = rr & 127u, bit = (tt >> 2) * myw;
+          const uint32_t word = mybase + (rr >> 7) * w4 + 4u * (bit >> 5) + (tt & 3u);
+          sh[j] = bit & 31u;
+          pp[j] = ldg_u8(ba + mybp + ee);
+          lo[j] = ldg_u32(page + (ok[j] ? word : 0u));
+          hi[j] = ldg_u32(page + (ok[j] ? word + (sh[j] + myw > 32 ? 4u : 0u) : 0u));
         }
-        // (b) consume: extract the highs and OR them into the tile
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (r0 + j < nr && 32u * (r0 + j) + lane < tot) {
-            const uint32_t k = ek[j] & 0xFFu, w = (ek[j] >> 8) & 0xFFu, b = ek[j] >> 16;
-            const uint32_t high = funnel_r(lo[j], hi[j], sh[j]) & low_mask(w);
+        for (int j = 0; j < 2; ++j) {
+          if (ok[j]) {
+            const uint32_t high = funnel_r(lo[j], hi[j], sh[j]) & wmask;
             if (pp[j] < 128u)
-              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(OutStage::swz(t, 128u * k + pp[j])),
-                           "r"(high << b));
+              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(OutStage::swz(t, 128u * q + pp[j])),
+                           "r"(high << myb));
             else
               bad = true;
           }
