@@ -324,16 +324,18 @@ __device__ int32_t fastpfor_core(WarpRing& r, OutStage& os, FpScratch& sc, const
   if (nw == 0) return IZG_E_FP_TRUNC_PAGE;
   const uint32_t A = ldg_u32(page);
   if (A < 1 || A >= nw) return IZG_E_FP_BA_OFFSET;
-  if (lane == 0) prefetch_l2(page + A, 4u * (nw - A));
   const uint32_t L = ldg_u32(page + A);
   const uint64_t ba_words = ((uint64_t)L + 3) / 4;
   if (A + 1 + ba_words > nw) return IZG_E_FP_TRUNC_BA;
   const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
 
+  const uint64_t keep = r.policy;
+  r.policy = policy_evict_last();  // the patch re-reads the position bytes
   r.begin(page + A + 1, (uint32_t)ba_words);
   uint32_t parsed = 0;
   int32_t st = fp_parse(r, sc, L, nblocks, lane, &parsed);
   r.end();
+  r.policy = keep;
   __syncwarp();  // table written by lane 0 -> visible to all lanes
   if (st) return fp_positions_bad(sc, ba, parsed, lane) ? IZG_E_FP_POS_RANGE : st;
 
@@ -341,6 +343,11 @@ __device__ int32_t fastpfor_core(WarpRing& r, OutStage& os, FpScratch& sc, const
   st = fp_directory(sc, page, nw, A + 1 + ba_words, lane, &end);
   if (st) return fp_positions_bad(sc, ba, nblocks, lane) ? IZG_E_FP_POS_RANGE : st;
 
+  // exception arrays: warm L2 while the packed area streams
+  if (lane == 0) {
+    const uint32_t x0 = A + 1 + (uint32_t)ba_words;
+    prefetch_l2(page + x0, 4u * (end - x0));
+  }
   r.begin(page + 1, A - 1);
   bool bad_pos = false;
   st = fp_blocks<DELTA>(r, os, sc, page, A, nblocks, out, oal, orow, carry, &bad_pos);
