@@ -147,6 +147,23 @@ int izg_decode(int codec, int delta, const uint32_t* d_words,
                const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
                int32_t* d_status, uint32_t* d_consumed, void* stream);
 
+/* Bytes of device workspace izg_decode_ws can use for n_chunks chunks of
+ * this codec (0 when the codec has no indexed path: SIMD-BP128). */
+uint64_t izg_decode_workspace_size(int codec, uint32_t n_chunks);
+
+/* izg_decode with a caller-owned device workspace (16-byte aligned, at least
+ * izg_decode_workspace_size bytes; otherwise this is exactly izg_decode).
+ * SIMD-FastPFOR then runs as two stream-ordered launches: a page index pass
+ * (one thread per page walks the byte array and the exception directory and
+ * makes every metadata check of codec_patched.cpp:292-416) and the fused
+ * decode reading per-block records.  Results and statuses are identical to
+ * izg_decode's; the workspace must stay untouched until the decode completes
+ * on `stream`. */
+int izg_decode_ws(int codec, int delta, const uint32_t* d_words,
+                  const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
+                  int32_t* d_status, uint32_t* d_consumed, void* d_workspace,
+                  uint64_t workspace_bytes, void* stream);
+
 /* Order-sensitive checksum of n words: sum over i of (w_i + 1) * (2i + 1)
  * mod 2^64 (xor of all words in d_result[1]).  Used for whole-box parity with
  * an NCCL reduction; not part of the reference. */

@@ -16,6 +16,7 @@
 #include "decode_bp128.cuh"
 #include "decode_fastpfor.cuh"
 #include "encode.cuh"
+#include "index_fastpfor.cuh"
 #include "izg_common.cuh"
 
 namespace izg {
@@ -35,13 +36,14 @@ __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t
 
 // Persistent kernel: every warp repeatedly claims the next chunk (one atomic
 // per chunk) and decodes it end to end: stream, unpack, patch, prefix sum,
-// VByte remainder, consumption check, status.
-template <int CODEC, int DELTA>
+// VByte remainder, consumption check, status.  IDX (SIMD-FastPFOR only):
+// pages were indexed by fp_index_kernel into `ix`.
+template <int CODEC, int DELTA, bool IDX>
 __global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32) __maxnreg__(Layout<CODEC>::kMaxRegs)
     decode_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                   uint32_t n_chunks, uint32_t* __restrict__ out, int32_t* __restrict__ status,
                   uint32_t* __restrict__ consumed, uint32_t* __restrict__ next_chunk,
-                  const __grid_constant__ CUtensorMap omap, int tma_out) {
+                  const __grid_constant__ CUtensorMap omap, int tma_out, IdxView ix) {
   extern __shared__ __align__(1024) uint8_t smem[];
   using LY = Layout<CODEC>;
   constexpr bool kArray = DELTA != IZG_DELTA_NONE;
@@ -88,6 +90,9 @@ __global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32) __maxnreg__(Layout
           st = bp128_core<DELTA, false>(r, os, ch.n_words, core / 128, o, oal, orow, carry,
                                         &pos);
         r.end();
+      } else if (IDX) {
+        st = fastpfor_core_idx<DELTA>(r, os, *fsc, p, c, core / 128, ix, o, oal, orow, carry,
+                                      &pos);
       } else {
         st = fastpfor_core<DELTA>(r, os, *fsc, p, ch.n_words, core / 128, o, oal, orow,
                                   carry, &pos);
@@ -139,7 +144,7 @@ __global__ void checksum_kernel(const uint32_t* __restrict__ d, uint64_t n,
 // ---- launch plumbing -------------------------------------------------------
 
 using KernelFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
-                          uint32_t*, uint32_t*, const CUtensorMap, int);
+                          uint32_t*, uint32_t*, const CUtensorMap, int, IdxView);
 
 // 2-D view of the output for TMA stores: rows of 32 integers (128 B), box
 // of 16 rows (one warp iteration), 128-byte swizzle.  The row extent is
@@ -169,14 +174,14 @@ bool make_out_map(CUtensorMap* m, uint32_t* out) {
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int CODEC>
+template <int CODEC, bool IDX>
 KernelFn pick(int delta) {
   switch (delta) {
-    case IZG_DELTA_NONE: return decode_kernel<CODEC, IZG_DELTA_NONE>;
-    case IZG_DELTA_D1: return decode_kernel<CODEC, IZG_DELTA_D1>;
-    case IZG_DELTA_D4: return decode_kernel<CODEC, IZG_DELTA_D4>;
-    case IZG_DELTA_D2: return decode_kernel<CODEC, IZG_DELTA_D2>;
-    case IZG_DELTA_DM: return decode_kernel<CODEC, IZG_DELTA_DM>;
+    case IZG_DELTA_NONE: return decode_kernel<CODEC, IZG_DELTA_NONE, IDX>;
+    case IZG_DELTA_D1: return decode_kernel<CODEC, IZG_DELTA_D1, IDX>;
+    case IZG_DELTA_D4: return decode_kernel<CODEC, IZG_DELTA_D4, IDX>;
+    case IZG_DELTA_D2: return decode_kernel<CODEC, IZG_DELTA_D2, IDX>;
+    case IZG_DELTA_DM: return decode_kernel<CODEC, IZG_DELTA_DM, IDX>;
   }
   return nullptr;
 }
@@ -189,7 +194,7 @@ struct DeviceInfo {
   bool init = false;
   bool ok = false;
   int sms = 0;
-  int occ[2][5] = {};
+  int occ[3][5] = {};  // [codec, or 2 = indexed SIMD-FastPFOR][delta]
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -208,7 +213,8 @@ int device_of(const void* p) {
   return a.device;
 }
 
-int prepare(int dev, int codec, int delta, KernelFn fn, int threads, size_t smem,
+// `variant` = codec, or 2 for the indexed SIMD-FastPFOR decode kernel.
+int prepare(int dev, int variant, int delta, KernelFn fn, int threads, size_t smem,
             int* grid_per_sm, int* sms, uint32_t** counter) {
   if (dev < 0 || dev >= 64) return IZG_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -225,7 +231,7 @@ int prepare(int dev, int codec, int delta, KernelFn fn, int threads, size_t smem
     }
   }
   if (!d.ok) return IZG_ERR_NO_DEVICE;
-  if (!d.occ[codec][delta]) {
+  if (!d.occ[variant][delta]) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return IZG_ERR_CUDA;
@@ -234,9 +240,9 @@ int prepare(int dev, int codec, int delta, KernelFn fn, int threads, size_t smem
             cudaSuccess ||
         occ < 1)
       return IZG_ERR_CUDA;
-    d.occ[codec][delta] = occ;
+    d.occ[variant][delta] = occ;
   }
-  *grid_per_sm = d.occ[codec][delta];
+  *grid_per_sm = d.occ[variant][delta];
   *sms = d.sms;
   *counter = d.counters + (d.next_slot++ % kCounterSlots);
   return IZG_SUCCESS;
@@ -257,10 +263,11 @@ struct DeviceGuard {
 
 }  // namespace izg
 
-extern "C" int izg_decode(int codec, int delta, const uint32_t* d_words,
-                          const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
-                          int32_t* d_status, uint32_t* d_consumed, void* stream) {
-  using namespace izg;
+namespace izg {
+
+int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* d_chunks,
+                uint32_t n_chunks, uint32_t* d_out, int32_t* d_status, uint32_t* d_consumed,
+                void* d_ws, uint64_t ws_bytes, void* stream) {
   if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return IZG_ERR_INVALID_ARGUMENT;
   if (delta < IZG_DELTA_NONE || delta > IZG_DELTA_DM) return IZG_ERR_INVALID_ARGUMENT;
   if (n_chunks == 0) return IZG_SUCCESS;
@@ -273,7 +280,12 @@ extern "C" int izg_decode(int codec, int delta, const uint32_t* d_words,
   }
   const int dev = device_of(d_status);
   if (dev < 0) return IZG_ERR_INVALID_ARGUMENT;
-  KernelFn fn = codec == IZG_SIMDBP128 ? pick<IZG_SIMDBP128>(delta) : pick<IZG_SIMDFASTPFOR>(delta);
+  const bool idx = codec == IZG_SIMDFASTPFOR && d_ws &&
+                   (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
+                   ws_bytes >= idx_workspace_bytes(n_chunks);
+  KernelFn fn = codec == IZG_SIMDBP128 ? pick<IZG_SIMDBP128, false>(delta)
+                : idx                  ? pick<IZG_SIMDFASTPFOR, true>(delta)
+                                       : pick<IZG_SIMDFASTPFOR, false>(delta);
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;
   uint32_t* counter = nullptr;
@@ -281,18 +293,58 @@ extern "C" int izg_decode(int codec, int delta, const uint32_t* d_words,
                                            : Layout<IZG_SIMDFASTPFOR>::kWarps;
   const size_t smem = codec == IZG_SIMDBP128 ? Layout<IZG_SIMDBP128>::kSmem
                                              : Layout<IZG_SIMDFASTPFOR>::kSmem;
-  int rc = prepare(dev, codec, delta, fn, warps * 32, smem, &per_sm, &sms, &counter);
+  int rc = prepare(dev, idx ? 2 : codec, delta, fn, warps * 32, smem, &per_sm, &sms, &counter);
   if (rc != IZG_SUCCESS) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  IdxView ix{};
+  if (idx) {
+    static const bool attr = [] {
+      cudaFuncSetAttribute(fp_index_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)IdxLayout::kSmem);
+      cudaFuncSetAttribute(fp_index_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)IdxLayout::kSmem);
+      return true;
+    }();
+    (void)attr;
+    ix = idx_view(d_ws, n_chunks);
+    const uint32_t g = (n_chunks + kIdxWarps - 1) / kIdxWarps;
+    if (delta == IZG_DELTA_NONE)
+      fp_index_kernel<false><<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks,
+                                                                         n_chunks, ix);
+    else
+      fp_index_kernel<true><<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks,
+                                                                        n_chunks, ix);
+  }
   const uint64_t want = (n_chunks + warps - 1) / warps;
   const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
   if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
   CUtensorMap omap;
   std::memset(&omap, 0, sizeof(omap));
   const int tma_out = make_out_map(&omap, d_out) ? 1 : 0;
-  fn<<<grid, warps * 32, smem, s>>>(d_words, d_chunks, n_chunks, d_out, d_status,
-                                          d_consumed, counter, omap, tma_out);
+  fn<<<grid, warps * 32, smem, s>>>(d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
+                                    counter, omap, tma_out, ix);
   return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+}
+
+}  // namespace izg
+
+extern "C" int izg_decode(int codec, int delta, const uint32_t* d_words,
+                          const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
+                          int32_t* d_status, uint32_t* d_consumed, void* stream) {
+  return izg::decode_impl(codec, delta, d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
+                          nullptr, 0, stream);
+}
+
+extern "C" uint64_t izg_decode_workspace_size(int codec, uint32_t n_chunks) {
+  return codec == IZG_SIMDFASTPFOR ? izg::idx_workspace_bytes(n_chunks) : 0;
+}
+
+extern "C" int izg_decode_ws(int codec, int delta, const uint32_t* d_words,
+                             const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
+                             int32_t* d_status, uint32_t* d_consumed, void* d_workspace,
+                             uint64_t workspace_bytes, void* stream) {
+  return izg::decode_impl(codec, delta, d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
+                          d_workspace, workspace_bytes, stream);
 }
 
 extern "C" int izg_checksum(const uint32_t* d_data, uint64_t n, uint64_t* d_result,

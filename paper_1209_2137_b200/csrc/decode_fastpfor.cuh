@@ -43,15 +43,18 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 // Per-warp scratch of the SIMD-FastPFOR decoder (shared memory).
 struct __align__(16) FpScratch {
   uint32_t tab[512];       // per block: b | w << 6 | c << 12 (w = maxbits - b)
+  uint32_t win[128];       // fp_parse: per window byte, len | len2 << 16
   uint32_t dir_base[33];   // by width w = 1..32
   uint32_t dir_n[33];
 };
 
 // Phase 1.  Walk of the byte array (codec_patched.cpp:309-336) in 128-byte
-// windows: lane l holds window bytes 4l..4l+3 and the speculative entry
-// length at each of them (2, or 3 + c when maxbits > b).  The serial chain of
-// entry starts then costs one shuffle per entry; up to 32 entries of a window
-// are validated and tabulated lane-parallel, and the first failing entry (in
+// windows.  Lane l decodes window bytes 4l..4l+3 as speculative entry starts:
+// len (2, or 3 + c when maxbits > b) and len2 = len + the len of the entry
+// that would follow (0 when that entry's header is not inside the window).
+// The serial chain of entry starts then reads one broadcast word from the
+// warp's window table per TWO entries; up to 32 entries of a window are
+// validated and tabulated lane-parallel, and the first failing entry (in
 // order) ends the walk with the reference's status.  *parsed = entries that
 // passed.
 __device__ int32_t fp_parse(WarpRing& r, FpScratch& sc, uint64_t L, uint32_t nblocks, int lane,
@@ -65,23 +68,37 @@ __device__ int32_t fp_parse(WarpRing& r, FpScratch& sc, uint64_t L, uint32_t nbl
     r.ensure(W + 128);
     const uint32_t word = lds32(r.base + ((r.ring_off() + W + 4u * lane) & kRingMask));
     const uint32_t nxt = __shfl_down_sync(0xFFFFFFFFu, word, 1);
-    uint32_t lens[2];
+    uint32_t len[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const uint32_t x = funnel_r(word, nxt, 8 * k);
       const uint32_t b = x & 0xFFu, mb = (x >> 8) & 0xFFu, c = (x >> 16) & 0xFFu;
-      const uint32_t len = mb > b ? 3 + c : 2;
-      if (k & 1) lens[k >> 1] |= len << 16; else lens[k >> 1] = len;
+      len[k] = mb > b ? 3 + c : 2;
     }
-    // serial chain of starts inside the window (uniform)
+    __syncwarp();  // previous window's chain is done with sc.win
+    reinterpret_cast<uint4*>(sc.win)[lane] = make_uint4(len[0], len[1], len[2], len[3]);
+    __syncwarp();
+    uint32_t pair[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t d2 = 4u * lane + k + len[k];  // the following entry's start
+      const uint32_t l2 = d2 <= 125 ? sc.win[d2] : 0u;
+      pair[k] = len[k] | (l2 ? len[k] + l2 : 0u) << 16;
+    }
+    __syncwarp();
+    reinterpret_cast<uint4*>(sc.win)[lane] = make_uint4(pair[0], pair[1], pair[2], pair[3]);
+    __syncwarp();
+    // serial chain of starts inside the window (uniform), two entries a step
     uint32_t m = 0, mystart = 0;
     const uint32_t cap = min(32u, nblocks - k0);
     while (m < cap && s <= W + 125) {
-      const uint32_t d = s - W;
-      const uint32_t v = __shfl_sync(0xFFFFFFFFu, (d & 2) ? lens[1] : lens[0], d >> 2);
+      const uint32_t v = sc.win[s - W];
+      const uint32_t l1 = v & 0xFFFFu, l2 = v >> 16;
       if ((uint32_t)lane == m) mystart = s;
-      s += (d & 1) ? v >> 16 : v & 0xFFFFu;
-      ++m;
+      const bool two = l2 != 0 && m + 1 < cap;
+      if (two && (uint32_t)lane == m + 1) mystart = s + l1;
+      s += two ? l2 : l1;
+      m += two ? 2u : 1u;
     }
     // lane-parallel checks of entries k0 .. k0+m-1, in the reference's order
     int32_t code = IZG_OK;
@@ -168,6 +185,54 @@ __device__ __forceinline__ uint32_t fp_high(const uint32_t* page, uint32_t base,
   return funnel_r(lo, hi, sh) & low_mask(w);
 }
 
+// Patch one warp iteration's exceptions into its output tile `t`
+// (codec_patched.cpp:390-404: o[pos] |= high << b).  Lanes 8q..8q+7 carry
+// block q's parameters (b, exception width w, count c, first position byte
+// bp in the byte array, cursor cur in array w, array base word) and patch
+// block q, sixteen exceptions per round with every load issued before the
+// first OR; the round count is set by the longest of the four lists.
+// Duplicate positions OR together like the reference.  Returns true when a
+// position >= 128 was met (the caller resolves precedence).
+__device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const uint8_t* ba,
+                                         uint32_t myb, uint32_t myw, uint32_t myc, uint32_t mybp,
+                                         uint32_t mycur, uint32_t mybase, int lane) {
+  const uint32_t q = (lane >> 3) & 3u, s8 = lane & 7;
+  uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));
+  mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));
+  const uint32_t wmask = low_mask(myw), w4 = 4u * myw;
+  bool bad = false;
+  for (uint32_t e0 = s8; e0 < mxc; e0 += 16) {
+    uint32_t pp[2], lo[2], hi[2], sh[2];
+    bool ok[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t e = e0 + 8u * j;
+      ok[j] = e < myc;
+      const uint32_t ee = ok[j] ? e : 0u;
+      const uint32_t rr = mycur + ee;
+      const uint32_t tt = rr & 127u, bit = (tt >> 2) * myw;
+      const uint32_t word = mybase + (rr >> 7) * w4 + 4u * (bit >> 5) + (tt & 3u);
+      sh[j] = bit & 31u;
+      // an idle slot reads the page's first words (always in bounds)
+      pp[j] = ok[j] ? ldg_u8(ba + mybp + ee) : 0u;
+      lo[j] = ldg_u32(page + (ok[j] ? word : 0u));
+      hi[j] = ldg_u32(page + (ok[j] ? word + (sh[j] + myw > 32 ? 4u : 0u) : 0u));
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      if (ok[j]) {
+        const uint32_t high = funnel_r(lo[j], hi[j], sh[j]) & wmask;
+        if (pp[j] < 128u)
+          asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(OutStage::swz(t, 128u * q + pp[j])),
+                       "r"(high << myb));
+        else
+          bad = true;
+      }
+    }
+  }
+  return bad;
+}
+
 // Phase 3.  Returns an izg_status; *bad_pos is set when a position >= 128
 // was met (the caller resolves precedence).
 template <int DELTA>
@@ -240,9 +305,6 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
     packed += __shfl_sync(0xFFFFFFFFu, pk, 3);
     bpos += __shfl_sync(0xFFFFFFFFu, bl, 3);
     const uint32_t tot = __shfl_sync(0xFFFFFFFFu, ce, 3);
-    // rounds of 8 exceptions per block: the longest list of the four
-    uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));
-    mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));
 
     // Stream window: packed words [first, packed) (the stream starts at word 1).
     r.release_below(4u * (first - 1));
@@ -258,37 +320,7 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
       const uint32_t t = os.acquire();
       OutStage::write(t, v, lane);
       __syncwarp();
-      // Lanes 8q..8q+7 patch block q, eight exceptions per round; two
-      // rounds per batch issue all their loads before the first OR.
-      const uint32_t wmask = low_mask(myw), w4 = 4u * myw;
-      for (uint32_t e0 = s8; e0 < mxc; e0 += 16) {
-        uint32_t pp[2], lo[2], hi[2], sh[2];
-        bool ok[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const uint32_t e = e0 + 8u * j;
-          ok[j] = e < myc;
-          const uint32_t ee = ok[j] ? e : 0u;  // myc == 0: loads stay in the page
-          const uint32_t rr = mycur + ee;
-          const uint32_t tt = rr & 127u, bit = (tt >> 2) * myw;
-          const uint32_t word = mybase + (rr >> 7) * w4 + 4u * (bit >> 5) + (tt & 3u);
-          sh[j] = bit & 31u;
-          pp[j] = ldg_u8(ba + mybp + ee);
-          lo[j] = ldg_u32(page + (ok[j] ? word : 0u));
-          hi[j] = ldg_u32(page + (ok[j] ? word + (sh[j] + myw > 32 ? 4u : 0u) : 0u));
-        }
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          if (ok[j]) {
-            const uint32_t high = funnel_r(lo[j], hi[j], sh[j]) & wmask;
-            if (pp[j] < 128u)
-              asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(OutStage::swz(t, 128u * q + pp[j])),
-                           "r"(high << myb));
-            else
-              bad = true;
-          }
-        }
-      }
+      bad |= fp_patch(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
       __syncwarp();
       OutStage::read(t, v, lane);
       scan<DELTA>(v, carry, lane);

@@ -99,6 +99,8 @@ struct Slot {
   uint32_t* out = nullptr;
   uint64_t out_cap = 0;
   int32_t* status = nullptr;
+  uint8_t* ws = nullptr;  // izg_decode_ws workspace (SIMD-FastPFOR index pass)
+  uint64_t ws_cap = 0;
 };
 
 struct Scratch {
@@ -120,6 +122,7 @@ struct Scratch {
       if (s.table) cudaFree(s.table);
       if (s.out) cudaFree(s.out);
       if (s.status) cudaFree(s.status);
+      if (s.ws) cudaFree(s.ws);
       if (s.stream) cudaStreamDestroy(s.stream);
       s = Slot{};
     }
@@ -224,8 +227,10 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     const uint64_t wcopy = std::min<uint64_t>(n_words, (whi + 3) & ~uint64_t{3}) - wlo;
     const uint64_t wneed = ((whi + 3) & ~uint64_t{3}) - wlo + 4;  // + the contract's pad row
     uint64_t tcap = s.table_cap;
+    const uint64_t wsb = izg_decode_workspace_size(codec, nc);
     if (!grow(s.words, s.words_cap, wneed) || !grow(s.table, tcap, nc) ||
-        !grow(s.out, s.out_cap, std::max<uint64_t>(ohi - olo, 1))) {
+        !grow(s.out, s.out_cap, std::max<uint64_t>(ohi - olo, 1)) ||
+        (wsb && !grow(s.ws, s.ws_cap, wsb))) {
       rc = IZG_ERR_CUDA;
       break;
     }
@@ -245,8 +250,8 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     cudaMemcpyAsync(s.table, S.pin_table + c0, sizeof(izg_chunk) * nc, cudaMemcpyHostToDevice,
                     s.stream);
     // Shifted base pointers: the kernel adds the table's absolute offsets.
-    const int r = izg_decode(codec, delta, s.words - wlo, s.table, nc, s.out - olo, s.status,
-                             nullptr, s.stream);
+    const int r = izg_decode_ws(codec, delta, s.words - wlo, s.table, nc, s.out - olo,
+                                s.status, nullptr, s.ws, wsb, s.stream);
     if (r != IZG_SUCCESS) {
       rc = r;
       break;

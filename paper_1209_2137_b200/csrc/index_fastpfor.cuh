@@ -1,0 +1,294 @@
+// index_fastpfor.cuh — page index pass of the two-kernel SIMD-FastPFOR path.
+//
+// The fused decoder (decode_fastpfor.cuh) spends about a quarter of its
+// instructions on the page's metadata: walking the byte array and turning
+// each block's entry into packed offsets, position offsets and per-width
+// exception cursors four blocks at a time.  With a workspace, izg_decode_ws
+// moves all of that into this kernel (one warp per page, 32 blocks per step,
+// at high occupancy), and the decode kernel reads one 16-byte record per
+// block instead.
+//
+// Per page one warp restates every check the reference makes before it
+// touches a packed word (codec_patched.cpp:292-416), in the reference's
+// order: page header (:296-305), the byte-array walk (:309-336, the fused
+// decoder's windowed fp_parse), the exception directory (:339-379) and the
+// block loop's overrun / exhaustion / packed-size checks (:381-415) over 32
+// blocks per step.  Exception positions are
+// NOT checked here — the decode kernel sees every position while patching,
+// and on error paths resolves POS_RANGE precedence from the records
+// (fp_positions_bad_idx), exactly as the fused path does.
+//
+// Workspace layout (izg_decode_workspace_size): for n chunks,
+//   hdr[n]        uint4 {status | parsed entries << 8, first word after the
+//                 byte array, end word (words consumed), A}
+//   dir[n][32]    uint32 base word of exception array w (index w-1)
+//   rec[n][512]   uint4 per block {b | w<<6 | c<<12, packed word, first
+//                 position byte (byte-array offset), cursor in array w}
+#pragma once
+#include "decode_fastpfor.cuh"
+#include "izg_common.cuh"
+
+namespace izg {
+
+constexpr uint32_t kMaxBlocks = IZG_CHUNK_SIZE / 128;  // 512 records per page
+
+struct IdxView {
+  uint4* hdr;
+  uint32_t* dir;
+  uint4* rec;
+  __device__ __forceinline__ uint4* page_rec(uint32_t c) const {
+    return rec + (size_t)c * kMaxBlocks;
+  }
+};
+
+__host__ __device__ inline uint64_t idx_workspace_bytes(uint32_t n_chunks) {
+  return (uint64_t)n_chunks * (16u + 32u * 4u + kMaxBlocks * 16u);
+}
+
+__host__ __device__ inline IdxView idx_view(void* ws, uint32_t n_chunks) {
+  IdxView v;
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  v.hdr = reinterpret_cast<uint4*>(p);
+  v.dir = reinterpret_cast<uint32_t*>(p + (size_t)n_chunks * 16u);
+  v.rec = reinterpret_cast<uint4*>(p + (size_t)n_chunks * (16u + 128u));
+  return v;
+}
+
+// Metadata pass over the parsed table, 32 blocks per step (lane = block):
+// packed word and first position byte (warp scans of 4b and entry lengths),
+// cursor in the block's width array (earlier same-width blocks of the step
+// plus the warp's running per-width count `cnt`), and — when `checks` — the
+// block loop's overrun / exhaustion checks in block order
+// (codec_patched.cpp:387-388, 406-407).  Records go out coalesced.
+__device__ int32_t fp_meta(const FpScratch& sc, uint32_t* cnt, uint4* rec, uint32_t nb,
+                           uint32_t A, bool checks, int lane, uint32_t* packed_end) {
+  cnt[lane + 1] = 0;
+  __syncwarp();
+  uint32_t packed = 1, bpos = 0;
+  int32_t err = IZG_OK;
+#pragma unroll 1
+  for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
+    const uint32_t k = j0 + lane;
+    const bool live = k < nb;
+    const uint32_t e = live ? sc.tab[k] : 0u;
+    const uint32_t b = e & 63u, w = (e >> 6) & 63u, c = e >> 12;
+    const uint32_t len = live ? (c ? 3 + c : 2u) : 0u;
+    const uint4 inc = warp_incl_scan<2>(make_uint4(4u * b, len, 0, 0), lane);
+    // exceptions of earlier same-width blocks of this step, by bit planes
+    const uint32_t grp = __match_any_sync(0xFFFFFFFFu, c ? w : 64u + lane);
+    const uint32_t below = grp & ((1u << lane) - 1u);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      acc += (uint32_t)__popc(__ballot_sync(0xFFFFFFFFu, (c >> j) & 1u) & below) << j;
+    const uint32_t cur = c ? cnt[w] + acc : 0u;
+    __syncwarp();
+    if (c && lane == 31 - __clz(grp)) cnt[w] = cur + c;  // last block of its width
+    __syncwarp();
+    if (checks && err == IZG_OK) {
+      const bool ov = live && packed + inc.x > A;
+      const bool ex = c && (uint64_t)cur + c > sc.dir_n[w];
+      const uint32_t bm = __ballot_sync(0xFFFFFFFFu, ov || ex);
+      if (bm) {
+        const int f = __ffs(bm) - 1;
+        err = (__ballot_sync(0xFFFFFFFFu, ov) >> f) & 1u ? IZG_E_FP_OVERRUN : IZG_E_FP_EXHAUSTED;
+      }
+    }
+    if (live) stg128_cg(rec + k, make_uint4(e, packed + inc.x - 4u * b, bpos + inc.y - len + 3u, cur));
+    packed += __shfl_sync(0xFFFFFFFFu, inc.x, 31);
+    bpos += __shfl_sync(0xFFFFFFFFu, inc.y, 31);
+  }
+  *packed_end = packed;
+  return err;
+}
+
+// Shared memory of the index kernel: per warp a TMA ring, an FpScratch, the
+// running per-width counts and the ring barriers.
+constexpr int kIdxWarps = 8;
+struct IdxLayout {
+  static constexpr uint32_t kScOff = kIdxWarps * kRingBytes;
+  static constexpr uint32_t kScBytes = (sizeof(FpScratch) + 15) & ~15u;
+  static constexpr uint32_t kCntOff = kScOff + kIdxWarps * kScBytes;
+  static constexpr uint32_t kBarOff = kCntOff + kIdxWarps * 36 * 4;
+  static constexpr size_t kSmem = kBarOff + kIdxWarps * kNS * 8;
+};
+
+// One warp indexes one page: header checks (codec_patched.cpp:296-305), the
+// windowed byte-array walk (fp_parse), the exception directory
+// (fp_directory), then fp_meta.  Statuses follow the reference's order;
+// positions are left to the decode kernel (see the file comment).
+template <bool ARRAY>
+__global__ void __launch_bounds__(kIdxWarps * 32)
+    fp_index_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
+                    uint32_t n_chunks, IdxView ix) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t c = blockIdx.x * kIdxWarps + warp;
+  if (c >= n_chunks) return;  // warp-uniform
+  const izg_chunk ch = chunks[c];
+  // decode_array's length check or decode_deltas' count checks: the decode
+  // kernel repeats them and never reads this page's record when they fail
+  if (ARRAY ? (ch.n == 0 || ch.n > IZG_CHUNK_SIZE) : (ch.n % 128 || ch.n > IZG_CHUNK_SIZE)) {
+    if (lane == 0) ix.hdr[c] = make_uint4(IZG_OK, 0, 0, 0);
+    return;
+  }
+  const uint32_t nblocks = (ARRAY ? ch.n / 128 * 128 : ch.n) / 128;
+  const uint32_t* page = words + ch.word_off;
+  const uint32_t nw = ch.n_words;
+  uint4 h = make_uint4(IZG_OK, 0, 0, 0);
+  if (nblocks == 0) {  // decode_deltas(count == 0) reads nothing (codec_patched.cpp:295)
+    if (lane == 0) ix.hdr[c] = h;
+    return;
+  }
+  const uint32_t A = nw ? __ldg(page) : 0u;
+  const uint32_t L = (nw && A >= 1 && A < nw) ? __ldg(page + A) : 0u;
+  const uint64_t ba_words = ((uint64_t)L + 3) / 4;
+  if (nw == 0) h.x = IZG_E_FP_TRUNC_PAGE;
+  else if (A < 1 || A >= nw) h.x = IZG_E_FP_BA_OFFSET;
+  else if (A + 1 + ba_words > nw) h.x = IZG_E_FP_TRUNC_BA;
+  if (h.x) {
+    if (lane == 0) ix.hdr[c] = h;
+    return;
+  }
+  WarpRing r;
+  r.gen = smem + warp * kRingBytes;
+  r.base = smem_u32(r.gen);
+  r.full = reinterpret_cast<uint64_t*>(smem + IdxLayout::kBarOff) + warp * kNS;
+  r.g = 0;
+  r.leader = lane == 0;
+  r.policy = policy_evict_last();  // the decode kernel re-reads the position bytes
+  FpScratch& sc = *reinterpret_cast<FpScratch*>(smem + IdxLayout::kScOff + warp * IdxLayout::kScBytes);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + IdxLayout::kCntOff) + warp * 36;
+  if (lane == 0) {
+    for (uint32_t i = 0; i < kNS; ++i) mbar_init(&r.full[i], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  r.begin(page + A + 1, (uint32_t)ba_words);
+  uint32_t parsed = 0;
+  int32_t st = fp_parse(r, sc, L, nblocks, lane, &parsed);
+  r.end();
+  __syncwarp();
+  uint32_t end = 0;
+  if (st == IZG_OK) {
+    st = fp_directory(sc, page, nw, A + 1 + ba_words, lane, &end);
+    if (st == IZG_OK) ix.dir[(size_t)c * 32 + lane] = sc.dir_base[lane + 1];
+  }
+  uint32_t packed = 0;
+  const int32_t bst = fp_meta(sc, cnt, ix.page_rec(c), parsed, A, st == IZG_OK, lane, &packed);
+  if (st == IZG_OK) st = bst ? bst : (packed != A ? IZG_E_FP_PACKED_SIZE : IZG_OK);
+  if (lane == 0) ix.hdr[c] = make_uint4((uint32_t)st | parsed << 8, A + 1 + (uint32_t)ba_words, end, A);
+}
+
+// ---- decode side -----------------------------------------------------------
+
+// Error paths: does any exception position of records [0, nb) reach 128
+// (codec_patched.cpp:328-330)?  Checked before every later error, as the
+// reference validates positions during its byte-array walk.
+__device__ bool fp_positions_bad_idx(const uint4* rec, const uint8_t* ba, uint32_t nb, int lane) {
+  bool bad = false;
+  for (uint32_t k = lane; k < nb; k += 32) {
+    const uint4 e = rec[k];
+    const uint32_t c = e.x >> 12;
+    for (uint32_t i = 0; i < c; ++i) bad |= ldg_u8(ba + e.z + i) >= 128u;
+  }
+  return __any_sync(0xFFFFFFFFu, bad);
+}
+
+// Blocks of an indexed page (codec_patched.cpp:381-415 minus the checks the
+// index pass already made): as fp_blocks, but each lane reads its block's
+// record (lanes 8q..8q+7 share block q's 16 bytes) one iteration ahead.
+// Returns true when an exception position >= 128 was met.
+template <int DELTA>
+__device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const FpScratch& sc, const uint4* rec,
+                              const uint32_t* page, uint32_t A, uint32_t nblocks, uint32_t* out,
+                              bool oal, int64_t orow, uint4& carry) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t q = lane >> 3, s8 = lane & 7;
+  const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
+  bool bad = false;
+  uint4 nx = rec[min(q, nblocks - 1)];
+#pragma unroll 1
+  for (uint32_t g0 = 0; g0 < nblocks; g0 += 4) {
+    const uint32_t ng = min(4u, nblocks - g0);
+    const bool live = q < ng;
+    const uint4 e = nx;
+    if (g0 + 4 < nblocks) nx = rec[min(g0 + 4 + q, nblocks - 1)];
+    const uint32_t myb = live ? e.x & 63u : 0u;
+    const uint32_t myw = (e.x >> 6) & 63u;
+    const uint32_t myc = live ? e.x >> 12 : 0u;
+    const uint32_t myoff = e.y, mybp = e.z, mycur = e.w;
+    const uint32_t first = __shfl_sync(0xFFFFFFFFu, myoff, 0);
+    const uint32_t after = __shfl_sync(0xFFFFFFFFu, myoff + 4u * myb, 8 * (ng - 1));
+    const bool tot = __any_sync(0xFFFFFFFFu, myc != 0);
+
+    // Stream window: packed words [first, after) (the stream starts at word 1).
+    r.release_below(4u * (first - 1));
+    r.ensure(4u * (after - 1));
+    uint32_t v[4][4];
+    if (r.phase == 0)
+      unpack_slots_aligned(r, r.ring_off() + 4u * (myoff - 1), myb, s8, v);
+    else
+      unpack_slots_unaligned(r, myoff - 1, myb, s8, v);
+    if (tot) {
+      const uint32_t mybase = sc.dir_base[myw];
+      const uint32_t t = os.acquire();
+      OutStage::write(t, v, lane);
+      __syncwarp();
+      bad |= fp_patch(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
+      __syncwarp();
+      OutStage::read(t, v, lane);
+      scan<DELTA>(v, carry, lane);
+      if (orow >= 0 && ng == 4) {
+        os.commit(v, lane, (uint32_t)(orow + 4 * g0));
+      } else {
+        os.abandon();
+        if (live) store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal);
+      }
+    } else {
+      scan<DELTA>(v, carry, lane);
+      if (orow >= 0 && ng == 4)
+        os.put(v, lane, (uint32_t)(orow + 4 * g0));
+      else if (live)
+        store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal);
+    }
+  }
+  return __any_sync(0xFFFFFFFFu, bad);
+}
+
+// Whole indexed page `c` (record written by fp_index_kernel); same contract
+// as fastpfor_core.
+template <int DELTA>
+__device__ int32_t fastpfor_core_idx(WarpRing& r, OutStage& os, FpScratch& sc,
+                                     const uint32_t* page, uint32_t c, uint32_t nblocks,
+                                     const IdxView& ix, uint32_t* out, bool oal, int64_t orow,
+                                     uint4& carry, uint32_t* pos_out) {
+  const int lane = threadIdx.x & 31;
+  if (nblocks == 0) {
+    *pos_out = 0;
+    return IZG_OK;
+  }
+  const uint4 h = ix.hdr[c];
+  const int32_t st = (int32_t)(h.x & 0xFFu);
+  const uint4* rec = ix.page_rec(c);
+  if (st) {
+    if (st == IZG_E_FP_TRUNC_PAGE || st == IZG_E_FP_BA_OFFSET || st == IZG_E_FP_TRUNC_BA)
+      return st;
+    return fp_positions_bad_idx(rec, reinterpret_cast<const uint8_t*>(page + h.w + 1), h.x >> 8,
+                                lane)
+               ? IZG_E_FP_POS_RANGE
+               : st;
+  }
+  const uint32_t A = h.w;
+  sc.dir_base[lane + 1] = ix.dir[(size_t)c * 32 + lane];
+  __syncwarp();
+  if (lane == 0) prefetch_l2(page + h.y, 4u * (h.z - h.y));  // exception arrays
+  r.begin(page + 1, A - 1);
+  const bool bad = fp_blocks_idx<DELTA>(r, os, sc, rec, page, A, nblocks, out, oal, orow, carry);
+  r.end();
+  if (bad) return IZG_E_FP_POS_RANGE;
+  *pos_out = h.z;
+  return IZG_OK;
+}
+
+}  // namespace izg

@@ -38,7 +38,7 @@ struct Layout {
   // registers per thread so that 3 CTAs fit in the 64K-register file
   static constexpr int kMaxRegs = CODEC == IZG_SIMDBP128 ? 80 : 96;
   // per-warp FpScratch (decode_fastpfor.cuh), 16-byte multiple
-  static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : 2048 + 2 * 33 * 4 + 8;
+  static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : 2048 + 512 + 2 * 33 * 4 + 8;
   static constexpr uint32_t kOutOff = kWarps * kRingBytes;
   static constexpr uint32_t kTabOff = kOutOff + kWarps * 2 * kStageOut;
   static constexpr uint32_t kBarOff = kTabOff + kWarps * kTabBytes;

@@ -102,6 +102,12 @@ __device__ __forceinline__ uint32_t lds8(uint32_t addr) {
 }
 
 // Streaming (evict-first) 16-byte global store for decoded output.
+// 16-byte store cached in L2 only (keeps L1 for the loads around it).
+__device__ __forceinline__ void stg128_cg(void* p, uint4 v) {
+  asm volatile("st.global.cg.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void stg128_cs(uint32_t* p, uint32_t a, uint32_t b, uint32_t c,
                                           uint32_t d) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c),

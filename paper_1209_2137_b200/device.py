@@ -12,10 +12,14 @@ from .codec import Codec, Encoded, raise_for_status
 
 
 class DeviceBatch:
-    """An Encoded batch resident in HBM plus its output and status buffers."""
+    """An Encoded batch resident in HBM plus its output and status buffers.
+
+    indexed=True gives SIMD-FastPFOR batches a decode workspace, so decode()
+    runs izg_decode_ws's two-launch path (page index pass + table-driven
+    decode); indexed=False keeps the single fused launch of izg_decode."""
 
     def __init__(self, codec: Codec, enc: Encoded, device=None, *, raw: bool = False,
-                 out=None):
+                 out=None, indexed: bool = True):
         import torch
 
         self.torch = torch
@@ -37,6 +41,9 @@ class DeviceBatch:
         self.consumed = torch.zeros(max(self.n_chunks, 1), dtype=torch.int32,
                                     device=self.device)
         self.sums = torch.zeros(2, dtype=torch.int64, device=self.device)
+        ws = N.lib().izg_decode_workspace_size(codec.codec, self.n_chunks) if indexed else 0
+        self.workspace = (torch.empty(ws, dtype=torch.uint8, device=self.device)
+                          if ws else None)
 
     @property
     def algorithmic_bytes(self) -> int:
@@ -45,9 +52,16 @@ class DeviceBatch:
 
     def decode(self, stream=None) -> None:
         s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
-        rc = N.lib().izg_decode(self.codec.codec, self.delta, N.ptr(self.words),
-                                N.ptr(self.table), self.n_chunks, N.ptr(self.out),
-                                N.ptr(self.status), N.ptr(self.consumed), s.cuda_stream)
+        if self.workspace is not None:
+            rc = N.lib().izg_decode_ws(self.codec.codec, self.delta, N.ptr(self.words),
+                                       N.ptr(self.table), self.n_chunks, N.ptr(self.out),
+                                       N.ptr(self.status), N.ptr(self.consumed),
+                                       N.ptr(self.workspace), self.workspace.numel(),
+                                       s.cuda_stream)
+        else:
+            rc = N.lib().izg_decode(self.codec.codec, self.delta, N.ptr(self.words),
+                                    N.ptr(self.table), self.n_chunks, N.ptr(self.out),
+                                    N.ptr(self.status), N.ptr(self.consumed), s.cuda_stream)
         if rc != N.SUCCESS:
             raise RuntimeError(f"izg_decode failed: {rc}")
 

@@ -1,0 +1,203 @@
+"""GPU parity of the two-launch SIMD-FastPFOR path (izg_decode_ws: page index
+pass + table-driven decode) against the single fused launch (izg_decode) and
+the oracle.
+
+Structural mutations target every metadata field of a page (codec_patched.cpp
+:292-416): the byte-array offset A, the byte-array length L, entry widths and
+counts, exception positions, the exception bitset and the per-width counts,
+and truncations at each region boundary.  Bar: identical per-chunk statuses
+and words consumed on both paths and in the oracle; identical outputs for
+every chunk that decodes.
+"""
+import zlib
+
+import numpy as np
+import pytest
+
+import paper_1209_2137_b200 as P
+from tests.helpers import random_sorted
+
+pytestmark = pytest.mark.gpu
+
+FP_NAMES = ["simdfastpfor", "simdfastpfor-s4", "simdfastpfor-d2", "simdfastpfor-dm"]
+
+
+def outlier_array(rng, n, rate=0.08):
+    gaps = rng.geometric(1 / 6, size=n).astype(np.uint64)
+    m = rng.random(n) < rate
+    gaps[m] = rng.integers(1 << 10, 1 << 22, size=int(m.sum()))
+    return np.minimum(np.cumsum(gaps), 0xFFFFFFFF).astype(np.uint32)
+
+
+def page_fields(p):
+    """(A, L, entry starts, exception-entry starts, directory word) of a page."""
+    A = int(p[0])
+    L = int(p[A])
+    ba = p[A + 1:].view(np.uint8)
+    starts, exc = [], []
+    s = 0
+    while s + 2 <= L:
+        b, mb = int(ba[s]), int(ba[s + 1])
+        starts.append(s)
+        if mb > b:
+            exc.append(s)
+            s += 3 + int(ba[s + 2])
+        else:
+            s += 2
+    return A, L, starts, exc, A + 1 + (L + 3) // 4
+
+
+def mutations(rng, p):
+    """Structural variants of one page payload (uint32 array)."""
+    A, L, starts, exc, bit_w = page_fields(p)
+    out = []
+
+    def var(f):
+        q = p.copy()
+        f(q, q[A + 1:].view(np.uint8))
+        out.append(q)
+
+    for d in (-1, 1, 5):
+        var(lambda q, ba, d=d: q.__setitem__(0, (A + d) & 0xFFFFFFFF))
+        var(lambda q, ba, d=d: q.__setitem__(A, (L + d) & 0xFFFFFFFF))
+    for s in (rng.choice(starts, size=min(6, len(starts)), replace=False) if starts else []):
+        var(lambda q, ba, s=s: ba.__setitem__(s, (int(ba[s]) + 1) % 40))      # b
+        var(lambda q, ba, s=s: ba.__setitem__(s + 1, (int(ba[s + 1]) + 3) % 40))  # maxbits
+    for s in (rng.choice(exc, size=min(6, len(exc)), replace=False) if exc else []):
+        c = int(p[A + 1:].view(np.uint8)[s + 2])
+        var(lambda q, ba, s=s: ba.__setitem__(s + 2, c + 1))                   # count
+        var(lambda q, ba, s=s: ba.__setitem__(s + 2, max(c - 1, 0)))
+        var(lambda q, ba, s=s: ba.__setitem__(s + 3 + int(rng.integers(0, c)),
+                                              128 + int(rng.integers(0, 128))))  # position
+    if bit_w < len(p):
+        bits = int(p[bit_w])
+        for k in (0, 3, 9):
+            var(lambda q, ba, k=k: q.__setitem__(bit_w, bits ^ (1 << k)))
+        if bit_w + 1 < len(p):
+            for d in (-1, 1, 200):
+                var(lambda q, ba, d=d: q.__setitem__(bit_w + 1, (int(p[bit_w + 1]) + d) & 0xFFFFFFFF))
+    for cut in {0, 1, A, A + 1, bit_w, bit_w + 1, bit_w + 2, len(p) - 1}:
+        if 0 <= cut < len(p):
+            out.append(p[:cut].copy())
+    return out
+
+
+def corpus(name, seed):
+    rng = np.random.default_rng(seed)
+    codec = P.make_codec(name)
+    payloads, counts = [], []
+    for n in (128, 700, 2048 + 130, 9000, 65536):
+        arr = outlier_array(rng, n)
+        p = P.encode_array(codec, arr)
+        payload = p.words[int(p.table["word_off"][0]):][:int(p.table["n_words"][0])].copy()
+        payloads.append(payload)
+        counts.append(n)
+        for q in mutations(rng, payload):
+            payloads.append(q)
+            counts.append(n)
+    return codec, payloads, counts
+
+
+def both_paths(codec, enc, raw=False):
+    res = []
+    for indexed in (False, True):
+        b = P.DeviceBatch(codec, enc, raw=raw, indexed=indexed)
+        assert (b.workspace is not None) == indexed
+        b.decode()
+        res.append((b.statuses(), b.output(), b.consumed[:b.n_chunks].cpu().numpy()))
+    return res
+
+
+@pytest.mark.parametrize("name", FP_NAMES)
+def test_structural_mutations_array(cuda, oracle, name):
+    codec, payloads, counts = corpus(name, zlib.crc32(name.encode()))
+    enc = P.layout(codec, payloads, counts)
+    (s0, o0, _), (s1, o1, _) = both_paths(codec, enc)
+    assert np.array_equal(s0, s1), np.nonzero(s0 != s1)[0][:10]
+    n_err = 0
+    for i, (p, n) in enumerate(zip(payloads, counts)):
+        ost, oout = oracle.decode_chunk(name, p, n)
+        assert s1[i] == ost, (i, s1[i], ost)
+        n_err += ost != 0
+        if ost == 0:
+            o = int(enc.table["out_off"][i])
+            assert np.array_equal(o1[o:o + n], oout), i
+            assert np.array_equal(o0[o:o + n], oout), i
+    assert n_err > len(payloads) // 2  # the corpus really is mostly corrupt
+    # the corpus reaches many FastPFOR status classes
+    seen = set(int(x) for x in s1) & set(range(9, 23))
+    assert len(seen) >= 6, seen
+
+
+@pytest.mark.parametrize("name", ["simdfastpfor", "simdfastpfor-s4"])
+def test_structural_mutations_raw(cuda, oracle, name):
+    """decode_deltas (codec.h:36-40): statuses and words consumed."""
+    rng = np.random.default_rng(7)
+    codec = P.make_codec(name)
+    payloads, counts = [], []
+    for n in (128, 1024, 65536):
+        deltas = outlier_array(rng, n) % (1 << 20)
+        p = oracle.encode_deltas(name, deltas)
+        payloads.append(p)
+        counts.append(n)
+        for q in mutations(rng, p):
+            payloads.append(q)
+            counts.append(n)
+    enc = P.layout(codec, payloads, counts)
+    (s0, o0, u0), (s1, o1, u1) = both_paths(codec, enc, raw=True)
+    assert np.array_equal(s0, s1)
+    assert np.array_equal(u0, u1)
+    for i, (p, n) in enumerate(zip(payloads, counts)):
+        ost, oout, used = oracle.decode_deltas(name, p, n)
+        assert s1[i] == ost, (i, s1[i], ost)
+        if ost == 0:
+            assert u1[i] == used
+            o = int(enc.table["out_off"][i])
+            assert np.array_equal(o1[o:o + n], oout), i
+
+
+@pytest.mark.parametrize("name", FP_NAMES)
+def test_random_byte_fuzz_both_paths(cuda, name):
+    codec = P.make_codec(name)
+    rng = np.random.default_rng(zlib.crc32(name.encode()) + 1)
+    payloads, counts = [], []
+    for rep in range(400):
+        n = int(rng.choice([300, 4096, 20000]))
+        arr = outlier_array(rng, n) if rep % 2 else random_sorted(rng, n, 3000)
+        e = P.encode_array(codec, arr)
+        p = e.words[int(e.table["word_off"][0]):][:int(e.table["n_words"][0])].copy()
+        b = p.view(np.uint8)
+        for _ in range(1 + rep % 3):
+            b[rng.integers(0, len(b))] = rng.integers(0, 256)
+        payloads.append(p)
+        counts.append(n)
+    enc = P.layout(codec, payloads, counts)
+    (s0, o0, _), (s1, o1, _) = both_paths(codec, enc)
+    assert np.array_equal(s0, s1)
+    for i, n in enumerate(counts):
+        if s1[i] == 0:
+            o = int(enc.table["out_off"][i])
+            assert np.array_equal(o0[o:o + n], o1[o:o + n]), i
+
+
+def test_workspace_too_small_falls_back_to_fused(cuda):
+    """izg_decode_ws with an undersized workspace is exactly izg_decode."""
+    import torch
+
+    from paper_1209_2137_b200 import _native as N
+
+    codec = P.make_codec("simdfastpfor-s4")
+    rng = np.random.default_rng(3)
+    arr = outlier_array(rng, 3 * 65536)
+    enc = P.encode_array(codec, arr)
+    b = P.DeviceBatch(codec, enc, indexed=False)
+    ws = torch.empty(64, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream()
+    rc = N.lib().izg_decode_ws(codec.codec, codec.delta, N.ptr(b.words), N.ptr(b.table),
+                               b.n_chunks, N.ptr(b.out), N.ptr(b.status), None, N.ptr(ws), 64,
+                               s.cuda_stream)
+    assert rc == N.SUCCESS
+    b.check()
+    assert np.array_equal(b.output(), arr)
+    assert N.lib().izg_decode_workspace_size(0, 100) == 0
+    assert N.lib().izg_decode_workspace_size(1, 100) == 100 * (16 + 128 + 512 * 16)

@@ -13,7 +13,7 @@ def run(name, model, count, d, seed=1, rate=0, reps=20, raw=False):
     enc = P.encode_chunks(codec, flat, offs, np.full(count, 65536, np.uint32),
                           allow_wrap=(model == "geometric"), raw=raw)
     t1 = time.time()
-    b = P.DeviceBatch(codec, enc, raw=raw)
+    b = P.DeviceBatch(codec, enc, raw=raw, indexed=os.environ.get("IZG_FUSED") != "1")
     for _ in range(3): b.decode()
     torch.cuda.synchronize(); b.check()
     if not raw:
