@@ -96,6 +96,18 @@ typedef enum izg_status {
   IZG_E_FP_OVERRUN = 20,       /* codec_patched.cpp:387-388 packed blocks overrun   */
   IZG_E_FP_EXHAUSTED = 21,     /* codec_patched.cpp:406-407 exception array exhausted */
   IZG_E_FP_PACKED_SIZE = 22,   /* codec_patched.cpp:414-415 packed area size mismatch */
+  /* INTZPK01 container reader, container.cpp (one status per container) */
+  IZG_E_CT_TRUNCATED = 23,     /* container.cpp:24-25,69-70,76-77 container: truncated */
+  IZG_E_CT_MAGIC = 24,         /* container.cpp:71       bad magic                 */
+  IZG_E_CT_NAME_LENGTH = 25,   /* container.cpp:73-74    bad codec name length     */
+  IZG_E_CT_FOUND_RAW = 26,     /* container.cpp:134-135  expected encoded data, found RAW */
+  IZG_E_CT_TRUNC_PAYLOAD = 27, /* container.cpp:47-48    truncated payload         */
+  IZG_E_CT_TRUNC_RECORD = 28,  /* container.cpp:147-148  truncated chunk record    */
+  IZG_E_CT_CHUNK_LENGTH = 29,  /* container.cpp:153-155  bad chunk length          */
+  IZG_E_CT_CHUNK_WORDS = 30,   /* container.cpp:156-157  bad chunk word count      */
+  IZG_E_CT_ARRAY_LENGTH = 31,  /* container.cpp:164-165  array length mismatch     */
+  IZG_E_CT_NOT_RAW = 32,       /* container.cpp:95-97    expected RAW data, found codec ... */
+  IZG_E_CT_RAW_COUNT = 33,     /* container.cpp:104-105  RAW word count mismatch   */
   /* misuse -> std::invalid_argument */
   IZG_E_COUNT_MULTIPLE = 64,   /* codec_binpack.cpp:13-14, codec_patched.cpp:53-54 count % 128 != 0 */
   IZG_E_PAGE_TOO_LARGE = 65,   /* codec_patched.cpp:55-56 page exceeds 65536 integers */
@@ -201,6 +213,46 @@ int izg_decode_host(int codec, int delta, const uint32_t* h_words,
 
 /* Release the per-thread device scratch used by the _host entry points. */
 void izg_release_host_scratch(void);
+
+/* ---- INTZPK01 container ingest (host) --------------------------------- */
+/* The reference's on-disk container (container.h:14-26) read from a host
+ * buffer instead of a std::istream, without copying payloads: chunk records
+ * are indexed in place, so the container body can be copied to the device
+ * as one block and decoded where it lies. */
+typedef struct izg_container {
+  char codec_name[260]; /* NUL-terminated; "RAW" for raw containers         */
+  uint32_t n_arrays;
+  uint32_t n_chunks;    /* chunk records (RAW: one per array)               */
+  uint64_t n_values;    /* sum of the arrays' lengths                       */
+  uint64_t body_offset; /* byte offset of the first array record            */
+  uint64_t body_words;  /* 32-bit words from body_offset through the last array */
+} izg_container;
+
+/* container_read_encoded (raw == 0, container.cpp:132-169) or
+ * container_read_raw (raw != 0, container.cpp:93-110) validation of
+ * buf[0, len): IZG_SUCCESS and *info, or IZG_ERR_CORRUPT with *status = the
+ * IZG_E_CT_* code of the reference's first CorruptError.  Trailing bytes
+ * after the last array are ignored, as by the reference. */
+int izg_container_scan(const void* buf, uint64_t len, int raw, izg_container* info,
+                       int32_t* status);
+
+/* Chunk table of a scanned container: chunks[k].word_off = index of chunk k's
+ * first payload word counted from body word 0 (the word at buf +
+ * info->body_offset), out_off consecutive over all arrays in order, so the
+ * arrays decode back to back.  array_chunk0 (nullable, n_arrays + 1 entries)
+ * receives each array's first chunk index.  RAW: one record per array
+ * covering its values. */
+int izg_container_index(const void* buf, uint64_t len, const izg_container* info,
+                        izg_chunk* chunks, uint32_t* array_chunk0);
+
+/* Read + decode a whole encoded container held in host memory: scan, index,
+ * then izg_decode_host of the body into h_out (n_values integers, arrays back
+ * to back).  *ct_status = container status (0 = OK); h_status (nullable,
+ * n_chunks entries) = per-chunk decode statuses.  Returns IZG_ERR_CORRUPT on
+ * any container or chunk error, IZG_ERR_UNKNOWN_CODEC for a codec without a
+ * device decoder (make_codec, codec.cpp:108). */
+int izg_container_decode_host(const void* buf, uint64_t len, uint32_t* h_out, uint64_t n_out,
+                              int32_t* ct_status, int32_t* h_status);
 
 #ifdef __cplusplus
 }

@@ -232,11 +232,91 @@ class Reference:
         L.izr_batch_output.argtypes = [vp, u32, vp]
         L.izr_batch_free.restype = None
         L.izr_batch_free.argtypes = [vp]
+        L.izr_container_write_encoded.restype = C.c_int
+        L.izr_container_write_encoded.argtypes = [cp, vp, vp, vp, u32, vp, u64, C.POINTER(u64),
+                                                  C.c_char_p, C.c_int]
+        L.izr_container_write_raw.restype = C.c_int
+        L.izr_container_write_raw.argtypes = [vp, vp, vp, u32, vp, u64, C.POINTER(u64),
+                                              C.c_char_p, C.c_int]
+        L.izr_container_read_encoded.restype = C.c_int
+        L.izr_container_read_encoded.argtypes = [vp, u64, C.c_char_p, C.c_int, vp, u64, vp, u32,
+                                                 vp, u32, C.POINTER(u32), C.POINTER(u32),
+                                                 C.c_char_p, C.c_int]
+        L.izr_container_read_raw.restype = C.c_int
+        L.izr_container_read_raw.argtypes = [vp, u64, vp, u64, vp, u32, C.POINTER(u32),
+                                             C.c_char_p, C.c_int]
 
     @staticmethod
     def _check(rc, err):
         if rc:
             raise RefError(rc, err.value.decode())
+
+    # ---- container.cpp -------------------------------------------------------
+
+    @staticmethod
+    def _arrays(arrays):
+        lens = np.array([len(a) for a in arrays], dtype=np.uint32)
+        offs = np.zeros(len(arrays), dtype=np.uint64)
+        if len(arrays) > 1:
+            offs[1:] = np.cumsum(lens[:-1], dtype=np.uint64)
+        flat = (np.concatenate([np.asarray(a, np.uint32) for a in arrays])
+                if arrays and lens.sum() else np.zeros(1, np.uint32))
+        return flat, offs, lens
+
+    def _write(self, fn, *args):
+        n = C.c_uint64()
+        err = C.create_string_buffer(256)
+        self._check(fn(*args, None, 0, C.byref(n), err, 256), err)
+        buf = np.zeros(max(n.value, 1), dtype=np.uint8)
+        self._check(fn(*args, _p(buf), len(buf), C.byref(n), err, 256), err)
+        return buf[:n.value].tobytes()
+
+    def container_write_encoded(self, name, arrays):
+        flat, offs, lens = self._arrays(arrays)
+        return self._write(self.L.izr_container_write_encoded, name.encode(), _p(flat), _p(offs),
+                           _p(lens) if len(lens) else None, len(arrays))
+
+    def container_write_raw(self, arrays):
+        flat, offs, lens = self._arrays(arrays)
+        return self._write(self.L.izr_container_write_raw, _p(flat), _p(offs),
+                           _p(lens) if len(lens) else None, len(arrays))
+
+    def container_read_encoded(self, data):
+        """(codec name, [[(original_length, payload words), ...] per array])."""
+        buf = np.frombuffer(bytes(data) + b"\0", dtype=np.uint8)
+        cap_w = len(data) // 4 + 1
+        words = np.zeros(cap_w, dtype=np.uint32)
+        table = np.zeros(cap_w, dtype=CHUNK_DTYPE)
+        c0 = np.zeros(len(data) // 8 + 2, dtype=np.uint32)
+        name = C.create_string_buffer(300)
+        na, nc = C.c_uint32(), C.c_uint32()
+        err = C.create_string_buffer(256)
+        rc = self.L.izr_container_read_encoded(_p(buf), len(data), name, 300, _p(words), cap_w,
+                                               _p(table), len(table), _p(c0), len(c0),
+                                               C.byref(na), C.byref(nc), err, 256)
+        self._check(rc, err)
+        out = []
+        for a in range(na.value):
+            out.append([(int(t["n"]), words[int(t["word_off"]):int(t["word_off"]) +
+                                            int(t["n_words"])].copy())
+                        for t in table[c0[a]:c0[a + 1]]])
+        return name.value.decode(), out
+
+    def container_read_raw(self, data):
+        buf = np.frombuffer(bytes(data) + b"\0", dtype=np.uint8)
+        cap = len(data) // 4 + 1
+        vals = np.zeros(cap, dtype=np.uint32)
+        lens = np.zeros(len(data) // 8 + 1, dtype=np.uint32)
+        na = C.c_uint32()
+        err = C.create_string_buffer(256)
+        rc = self.L.izr_container_read_raw(_p(buf), len(data), _p(vals), cap, _p(lens), len(lens),
+                                           C.byref(na), err, 256)
+        self._check(rc, err)
+        out, pos = [], 0
+        for n in lens[:na.value]:
+            out.append(vals[pos:pos + int(n)].copy())
+            pos += int(n)
+        return out
 
     def encode_array(self, name, values):
         values = np.ascontiguousarray(values, dtype=np.uint32)

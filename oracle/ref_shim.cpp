@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -23,6 +24,7 @@
 #include "intzip/codec.h"
 #include "intzip/codec_basic.h"
 #include "intzip/codec_patched.h"
+#include "intzip/container.h"
 #include "intzip/datagen.h"
 #include "intzip/delta.h"
 #include "intzip/errors.h"
@@ -305,5 +307,98 @@ int izr_batch_output(void* handle, uint32_t i, uint32_t* out) {
 }
 
 void izr_batch_free(void* handle) { delete static_cast<Batch*>(handle); }
+
+// ---- container (container.cpp) -------------------------------------------
+
+// container_write_encoded over encode_array of each array (values of array i
+// at values[offs[i] .. offs[i] + lens[i])).  *len_out = bytes written (the
+// buffer may be null to size it).
+int izr_container_write_encoded(const char* name, const uint32_t* values,
+                                const uint64_t* offs, const uint32_t* lens,
+                                uint32_t n_arrays, uint8_t* buf, uint64_t cap,
+                                uint64_t* len_out, char* err, int errcap) {
+  return guarded(err, errcap, [&] {
+    const auto codec = intzip::make_codec(name);
+    std::vector<std::vector<intzip::Chunk>> arrays(n_arrays);
+    for (uint32_t i = 0; i < n_arrays; ++i)
+      arrays[i] = intzip::encode_array(*codec, {values + offs[i], lens[i]});
+    std::ostringstream os;
+    intzip::container_write_encoded(os, codec->name(), arrays);
+    const std::string s = os.str();
+    *len_out = s.size();
+    if (buf) {
+      if (s.size() > cap) throw std::runtime_error("buffer too small");
+      std::memcpy(buf, s.data(), s.size());
+    }
+  });
+}
+
+int izr_container_write_raw(const uint32_t* values, const uint64_t* offs,
+                            const uint32_t* lens, uint32_t n_arrays, uint8_t* buf,
+                            uint64_t cap, uint64_t* len_out, char* err, int errcap) {
+  return guarded(err, errcap, [&] {
+    std::vector<std::vector<uint32_t>> arrays(n_arrays);
+    for (uint32_t i = 0; i < n_arrays; ++i)
+      arrays[i].assign(values + offs[i], values + offs[i] + lens[i]);
+    std::ostringstream os;
+    intzip::container_write_raw(os, arrays);
+    const std::string s = os.str();
+    *len_out = s.size();
+    if (buf) {
+      if (s.size() > cap) throw std::runtime_error("buffer too small");
+      std::memcpy(buf, s.data(), s.size());
+    }
+  });
+}
+
+// container_read_encoded: codec name, then every chunk's payload packed back
+// to back into `words` with its record in `chunks` (out_off consecutive over
+// all arrays) and array i's first chunk at array_chunk0[i].
+int izr_container_read_encoded(const uint8_t* buf, uint64_t len, char* name, int namecap,
+                               uint32_t* words, uint64_t words_cap, ChunkRec* chunks,
+                               uint32_t chunks_cap, uint32_t* array_chunk0,
+                               uint32_t arrays_cap, uint32_t* n_arrays, uint32_t* n_chunks,
+                               char* err, int errcap) {
+  return guarded(err, errcap, [&] {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(buf), len));
+    const intzip::EncodedContainer c = intzip::container_read_encoded(is);
+    set_err(name, namecap, c.codec_name.c_str());
+    if (c.arrays.size() + 1 > arrays_cap) throw std::runtime_error("array table too small");
+    uint64_t pos = 0, out = 0;
+    uint32_t k = 0;
+    for (size_t a = 0; a < c.arrays.size(); ++a) {
+      array_chunk0[a] = k;
+      for (const intzip::Chunk& ch : c.arrays[a]) {
+        if (k >= chunks_cap || pos + ch.payload.size() > words_cap)
+          throw std::runtime_error("output too small");
+        std::memcpy(words + pos, ch.payload.data(), ch.payload.size() * 4);
+        chunks[k++] = {pos, static_cast<uint32_t>(ch.payload.size()), ch.original_length, out};
+        pos += ch.payload.size();
+        out += ch.original_length;
+      }
+    }
+    array_chunk0[c.arrays.size()] = k;
+    *n_arrays = static_cast<uint32_t>(c.arrays.size());
+    *n_chunks = k;
+  });
+}
+
+int izr_container_read_raw(const uint8_t* buf, uint64_t len, uint32_t* values, uint64_t cap,
+                           uint32_t* lens, uint32_t lens_cap, uint32_t* n_arrays, char* err,
+                           int errcap) {
+  return guarded(err, errcap, [&] {
+    std::istringstream is(std::string(reinterpret_cast<const char*>(buf), len));
+    const auto arrays = intzip::container_read_raw(is);
+    if (arrays.size() > lens_cap) throw std::runtime_error("array table too small");
+    uint64_t pos = 0;
+    for (size_t a = 0; a < arrays.size(); ++a) {
+      if (pos + arrays[a].size() > cap) throw std::runtime_error("output too small");
+      std::memcpy(values + pos, arrays[a].data(), arrays[a].size() * 4);
+      lens[a] = static_cast<uint32_t>(arrays[a].size());
+      pos += arrays[a].size();
+    }
+    *n_arrays = static_cast<uint32_t>(arrays.size());
+  });
+}
 
 }  // extern "C"

@@ -7,8 +7,12 @@ from . import _native
 from .codec import (CHUNK_SIZE, Codec, CorruptError, Encoded, codec_names, decode_array,
                     encode_array, encode_chunks, gen_arrays, layout, make_codec,
                     raise_for_status)
+from .container import (Container, decode_container, read_container, read_raw_container,
+                        scan_container)
 from .device import DeviceBatch
 
-__all__ = ["CHUNK_SIZE", "Codec", "CorruptError", "DeviceBatch", "Encoded", "codec_names",
+__all__ = ["CHUNK_SIZE", "Codec", "Container", "CorruptError", "DeviceBatch", "Encoded",
+           "codec_names", "decode_container", "read_container", "read_raw_container",
+           "scan_container",
            "decode_array", "encode_array", "encode_chunks", "gen_arrays", "layout",
            "make_codec", "raise_for_status", "_native"]

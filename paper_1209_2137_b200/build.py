@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libintzip_b200.so")
 
-SOURCES = ["decode.cu", "host.cpp", "host_encode.cpp", "host_datagen.cpp"]
+SOURCES = ["decode.cu", "host.cpp", "host_encode.cpp", "host_datagen.cpp", "container.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",

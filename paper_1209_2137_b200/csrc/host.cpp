@@ -36,6 +36,17 @@ extern "C" const char* izg_status_string(int32_t s) {
     case IZG_E_FP_OVERRUN: return "fastpfor: packed blocks overrun byte array";
     case IZG_E_FP_EXHAUSTED: return "fastpfor: exception array exhausted";
     case IZG_E_FP_PACKED_SIZE: return "fastpfor: packed area size mismatch";
+    case IZG_E_CT_TRUNCATED: return "container: truncated";
+    case IZG_E_CT_MAGIC: return "container: bad magic";
+    case IZG_E_CT_NAME_LENGTH: return "container: bad codec name length";
+    case IZG_E_CT_FOUND_RAW: return "container: expected encoded data, found RAW";
+    case IZG_E_CT_TRUNC_PAYLOAD: return "container: truncated payload";
+    case IZG_E_CT_TRUNC_RECORD: return "container: truncated chunk record";
+    case IZG_E_CT_CHUNK_LENGTH: return "container: bad chunk length";
+    case IZG_E_CT_CHUNK_WORDS: return "container: bad chunk word count";
+    case IZG_E_CT_ARRAY_LENGTH: return "container: array length mismatch";
+    case IZG_E_CT_NOT_RAW: return "container: expected RAW data, found codec";
+    case IZG_E_CT_RAW_COUNT: return "container: RAW word count mismatch";
     case IZG_E_COUNT_MULTIPLE: return "count must be a multiple of 128";
     case IZG_E_PAGE_TOO_LARGE: return "patched codec: page exceeds 65536 integers";
     case IZG_E_DECREASING: return "delta encode: input is not nondecreasing";

@@ -46,6 +46,12 @@ class DeviceBatch:
                           if ws else None)
 
     @property
+    def launches_per_decode(self) -> int:
+        """Kernels one decode() launches (memsets excluded): the indexed
+        SIMD-FastPFOR path runs the page index pass, then the decode."""
+        return 2 if self.workspace is not None else 1
+
+    @property
     def algorithmic_bytes(self) -> int:
         """Compressed bytes read + 4 B per decoded integer."""
         return 4 * self.payload_words + 4 * self.n_out

@@ -81,6 +81,16 @@ def main():
         out[f"bad/{name}/nwords"] = np.array([len(p) for p in pays], np.uint32)
         out[f"bad/{name}/status"] = np.array(stats, np.int32)
         out[f"bad/{name}/decoded"] = np.stack(decs)
+    # an INTZPK01 container written by the reference (container.cpp:112-130)
+    # and the chunk table its reader returns (container.cpp:132-169)
+    crng = np.random.default_rng(20240)
+    arrays = [random_sorted(crng, n, 3000) for n in (0, 7, 129, 70000)]
+    data = ref.container_write_encoded("simdbp128-s4", arrays)
+    _, rarr = ref.container_read_encoded(data)
+    out["container_bytes"] = np.frombuffer(data, dtype=np.uint8)
+    out["container_n"] = np.array([n for a in rarr for n, _ in a], np.uint32)
+    out["container_n_words"] = np.array([len(p) for a in rarr for _, p in a], np.uint32)
+    out["container_values"] = np.concatenate(arrays)
     np.savez_compressed(os.path.join(HERE, "ref_vectors.npz"), **out)
     print("wrote", len(out), "arrays")
 
