@@ -35,10 +35,16 @@ extern "C" {
 /* Chunk length cap: intzip::kChunkSize (codec.h:17). */
 #define IZG_CHUNK_SIZE 65536u
 
-/* Codec formats on the hot path (codec_binpack.h:17-25, codec_patched.h:69-85). */
+/* Codec formats (codec_binpack.h:10-25, codec_patched.h:59-80).  The hot
+ * path is SIMD-BP128 and SIMD-FastPFOR; BP32, FastPFOR (scalar groups) and
+ * SimplePFOR (Simple-8b exception highs) are the same page framework with
+ * scalar 32-integer groups: decode only. */
 typedef enum izg_codec {
   IZG_SIMDBP128 = 0,
-  IZG_SIMDFASTPFOR = 1
+  IZG_SIMDFASTPFOR = 1,
+  IZG_BP32 = 2,
+  IZG_FASTPFOR = 3,
+  IZG_SIMPLEPFOR = 4
 } izg_codec;
 
 /* Inverse differential coding fused into decode.
@@ -108,6 +114,12 @@ typedef enum izg_status {
   IZG_E_CT_ARRAY_LENGTH = 31,  /* container.cpp:164-165  array length mismatch     */
   IZG_E_CT_NOT_RAW = 32,       /* container.cpp:95-97    expected RAW data, found codec ... */
   IZG_E_CT_RAW_COUNT = 33,     /* container.cpp:104-105  RAW word count mismatch   */
+  /* BP32, codec_binpack.cpp */
+  IZG_E_BP32_TRUNC_DESC = 34,  /* codec_binpack.cpp:46-47 bp32: truncated descriptor */
+  IZG_E_BP32_WIDTH = 35,       /* codec_binpack.cpp:51    bp32: width byte exceeds 32 */
+  IZG_E_BP32_TRUNC_PAYLOAD = 36, /* codec_binpack.cpp:52-53 bp32: truncated payload  */
+  /* SimplePFOR exception highs, codec_basic.cpp */
+  IZG_E_S8_EXHAUSTED = 37,     /* codec_basic.cpp:302-303 simple8b: stream exhausted before count */
   /* misuse -> std::invalid_argument */
   IZG_E_COUNT_MULTIPLE = 64,   /* codec_binpack.cpp:13-14, codec_patched.cpp:53-54 count % 128 != 0 */
   IZG_E_PAGE_TOO_LARGE = 65,   /* codec_patched.cpp:55-56 page exceeds 65536 integers */

@@ -39,6 +39,19 @@ void orc_unpack_vertical128(const uint32_t* words, uint32_t b, uint32_t* out) {
 }
 
 /* pack128<B> with masking (bitpack.cpp:87-120, 318-322): v mod 2^b. */
+/* bitpack.h:12-16 scalar layout, unpack_scalar32 (bitpack.cpp:305-309):
+ * value i at bits [i*b, i*b+b) of the b-word stream, low bits first. */
+void orc_unpack_scalar32(const uint32_t* words, uint32_t b, uint32_t* out) {
+  for (uint32_t i = 0; i < 32; ++i) {
+    uint64_t v = 0;
+    for (uint32_t k = 0; k < b; ++k) {
+      const uint32_t bit = i * b + k;
+      v |= (uint64_t)((words[bit / 32] >> (bit % 32)) & 1u) << k;
+    }
+    out[i] = (uint32_t)v;
+  }
+}
+
 void orc_pack_vertical128(const uint32_t* values, uint32_t b, uint32_t* out) {
   memset(out, 0, sizeof(uint32_t) * 4 * b);
   for (uint32_t t = 0; t < 128; ++t) {
@@ -252,6 +265,51 @@ static int bp128_decode(const uint32_t* words, size_t nwords, uint32_t* out,
   return IZG_OK;
 }
 
+/* Bp32Codec::decode_deltas (codec_binpack.cpp:43-60): per 128 integers one
+ * descriptor word (byte g = width of scalar group g), then 4 groups. */
+static int bp32_decode(const uint32_t* words, size_t nwords, uint32_t* out, size_t count,
+                       size_t* consumed) {
+  size_t pos = 0;
+  for (size_t base = 0; base < count; base += 128) {
+    if (pos >= nwords) return IZG_E_BP32_TRUNC_DESC;
+    const uint32_t desc = words[pos++];
+    for (int g = 0; g < 4; ++g) {
+      const uint32_t w = (desc >> (8 * g)) & 0xFF;
+      if (w > 32) return IZG_E_BP32_WIDTH;
+      if (pos + w > nwords) return IZG_E_BP32_TRUNC_PAYLOAD;
+      orc_unpack_scalar32(words + pos, w, out + base + 32 * g);
+      pos += w;
+    }
+  }
+  *consumed = pos;
+  return IZG_OK;
+}
+
+/* simple8b_decode, 32-bit overload (codec_basic.cpp:256-300, table
+ * codec_basic.h:45-60): 64-bit words, low half first; selector = low 4 bits;
+ * values truncated to 32 bits; returns words consumed or (size_t)-1 when the
+ * stream ends before `count` values. */
+static const uint32_t kS8Cap[16] = {240, 120, 60, 30, 20, 15, 12, 10, 8, 7, 6, 5, 4, 3, 2, 1};
+static const uint32_t kS8Bits[16] = {0, 0, 1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 15, 20, 30, 60};
+static size_t simple8b_decode(const uint32_t* words, size_t nwords, uint32_t* out,
+                              size_t count) {
+  size_t pos = 0, done = 0;
+  while (done < count) {
+    if (pos + 2 > nwords) return (size_t)-1;
+    const uint64_t word = words[pos] | ((uint64_t)words[pos + 1] << 32);
+    pos += 2;
+    const uint32_t sel = (uint32_t)(word & 0xF), bits = kS8Bits[sel];
+    size_t take = count - done < kS8Cap[sel] ? count - done : kS8Cap[sel];
+    for (size_t k = 0; k < take; ++k) {
+      uint64_t v = 0;
+      if (bits) v = (word >> (4 + k * bits)) & ((bits == 64 ? 0 : (1ull << bits)) - 1);
+      out[done + k] = (uint32_t)v;
+    }
+    done += take;
+  }
+  return pos;
+}
+
 /* FastPforCodec::encode_deltas, vertical_arrays storage
  * (codec_patched.cpp:219-290). */
 static size_t fastpfor_encode(const uint32_t* d, size_t count, uint32_t* out) {
@@ -308,9 +366,11 @@ static size_t fastpfor_encode(const uint32_t* d, size_t count, uint32_t* out) {
   return pos;
 }
 
-/* FastPforCodec::decode_deltas, vertical_arrays storage
- * (codec_patched.cpp:292-417), checks in the reference's order. */
-static int fastpfor_decode(const uint32_t* words, size_t nwords, uint32_t* out,
+/* FastPforCodec::decode_deltas (codec_patched.cpp:292-417) for the three
+ * patch storages (codec_patched.cpp:195-199): storage 0 = vertical_arrays
+ * (simdfastpfor), 1 = scalar_arrays (fastpfor), 2 = simple8b (simplepfor).
+ * Checks in the reference's order. */
+static int fastpfor_decode(int storage, const uint32_t* words, size_t nwords, uint32_t* out,
                            size_t count, size_t* consumed) {
   if (count == 0) { *consumed = 0; return IZG_OK; }
   const size_t blocks = count / 128;
@@ -345,41 +405,70 @@ static int fastpfor_decode(const uint32_t* words, size_t nwords, uint32_t* out,
   }
   if (bpos != ba_len) return IZG_E_FP_BA_LEN;
 
-  /* Exception directory: bitset, then per width its count and 16 B-aligned
-   * vertical groups (codec_patched.cpp:338-379).  Values are extracted on
-   * demand below instead of bulk-unpacked; the result is identical. */
+  /* Exception highs (codec_patched.cpp:338-379).  Arrays: bitset, then per
+   * width its count and its groups (vertical: 16 B-aligned groups of 128;
+   * scalar: groups of 32); values are extracted on demand below instead of
+   * bulk-unpacked, with identical results.  Simple-8b: one stream of all
+   * highs in block order. */
   size_t pos = ba_offset + 1 + ba_words;
   size_t arr_base[33] = {0}, arr_n[33] = {0};
-  if (pos >= nwords) return IZG_E_FP_NO_BITSET;
-  const uint32_t bitset = words[pos++];
-  for (uint32_t w = 1; w <= 32; ++w) {
-    if (!(bitset & (1u << (w - 1)))) continue;
-    if (pos >= nwords) return IZG_E_FP_TRUNC_EXC;
-    const uint32_t n = words[pos++];
-    while (pos % 4 != 0) ++pos;
-    const size_t padded = ((size_t)n + 127) / 128 * 128;
-    const size_t nw = padded / 128 * 4 * (size_t)w;
-    if (pos + nw > nwords) return IZG_E_FP_TRUNC_EXC;
-    arr_base[w] = pos;
-    arr_n[w] = n;
-    pos += nw;
+  static uint32_t s8_highs[512 * 255];
+  if (storage == 2) {
+    size_t total = 0;
+    for (size_t k = 0; k < blocks; ++k) total += mc[k];
+    const size_t used = simple8b_decode(words + pos, nwords - pos, s8_highs, total);
+    if (used == (size_t)-1) return IZG_E_S8_EXHAUSTED;
+    pos += used;
+  } else {
+    if (pos >= nwords) return IZG_E_FP_NO_BITSET;
+    const uint32_t bitset = words[pos++];
+    for (uint32_t w = 1; w <= 32; ++w) {
+      if (!(bitset & (1u << (w - 1)))) continue;
+      if (pos >= nwords) return IZG_E_FP_TRUNC_EXC;
+      const uint32_t n = words[pos++];
+      const size_t group = storage == 0 ? 128 : 32;
+      if (storage == 0)
+        while (pos % 4 != 0) ++pos;
+      const size_t padded = ((size_t)n + group - 1) / group * group;
+      const size_t nw = padded / group * (group / 32) * (size_t)w;
+      if (pos + nw > nwords) return IZG_E_FP_TRUNC_EXC;
+      arr_base[w] = pos;
+      arr_n[w] = n;
+      pos += nw;
+    }
   }
 
-  size_t packed = 1;
+  size_t packed = 1, s8_cursor = 0;
   size_t cursors[33] = {0};
   for (size_t k = 0; k < blocks; ++k) {
     if (packed + 4 * (size_t)mb[k] > ba_offset) return IZG_E_FP_OVERRUN;
     uint32_t* o = out + 128 * k;
-    orc_unpack_vertical128(words + packed, mb[k], o);
+    if (storage == 0) {
+      orc_unpack_vertical128(words + packed, mb[k], o);
+    } else {
+      for (int g = 0; g < 4; ++g)
+        orc_unpack_scalar32(words + packed + (size_t)mb[k] * g, mb[k], o + 32 * g);
+    }
     packed += 4 * (size_t)mb[k];
     if (mc[k]) {
       const uint32_t w = mmax[k] - mb[k];
       for (uint32_t i = 0; i < mc[k]; ++i) {
-        if (cursors[w] >= arr_n[w]) return IZG_E_FP_EXHAUSTED;
-        const size_t r = cursors[w]++;
-        uint32_t group[128];
-        orc_unpack_vertical128(words + arr_base[w] + (r / 128) * 4 * w, w, group);
-        o[bytes[mpos[k] + i]] |= group[r % 128] << mb[k];
+        uint32_t high;
+        if (storage == 2) {
+          high = s8_highs[s8_cursor++];
+        } else {
+          if (cursors[w] >= arr_n[w]) return IZG_E_FP_EXHAUSTED;
+          const size_t r = cursors[w]++;
+          uint32_t group[128];
+          if (storage == 0) {
+            orc_unpack_vertical128(words + arr_base[w] + (r / 128) * 4 * w, w, group);
+            high = group[r % 128];
+          } else {
+            orc_unpack_scalar32(words + arr_base[w] + (r / 32) * w, w, group);
+            high = group[r % 32];
+          }
+        }
+        o[bytes[mpos[k] + i]] |= high << mb[k];
       }
     }
   }
@@ -389,7 +478,7 @@ static int fastpfor_decode(const uint32_t* words, size_t nwords, uint32_t* out,
 }
 
 size_t orc_encode_deltas(int codec, const uint32_t* deltas, size_t count, uint32_t* out) {
-  if (count % 128 != 0) return (size_t)-1;
+  if (count % 128 != 0 || codec > IZG_SIMDFASTPFOR) return (size_t)-1;
   if (codec == IZG_SIMDBP128) return bp128_encode(deltas, count, out);
   if (count > 65536) return (size_t)-1;
   return fastpfor_encode(deltas, count, out);
@@ -399,8 +488,10 @@ int orc_decode_deltas(int codec, const uint32_t* words, size_t nwords,
                       uint32_t* out, size_t count, size_t* consumed) {
   if (count % 128 != 0) return IZG_E_COUNT_MULTIPLE;
   if (codec == IZG_SIMDBP128) return bp128_decode(words, nwords, out, count, consumed);
+  if (codec == IZG_BP32) return bp32_decode(words, nwords, out, count, consumed);
   if (count > 65536) return IZG_E_PAGE_TOO_LARGE;
-  return fastpfor_decode(words, nwords, out, count, consumed);
+  const int storage = codec == IZG_SIMDFASTPFOR ? 0 : codec == IZG_FASTPFOR ? 1 : 2;
+  return fastpfor_decode(storage, words, nwords, out, count, consumed);
 }
 
 /* ---- pipeline, one chunk (codec.cpp:14-69) ------------------------------ */

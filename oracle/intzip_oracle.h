@@ -27,6 +27,8 @@ uint32_t orc_max_bitwidth(const uint32_t* values, size_t n);
  * 87-120 / 318-322 (masked pack) */
 void orc_unpack_vertical128(const uint32_t* words, uint32_t b, uint32_t* out);
 void orc_pack_vertical128(const uint32_t* values, uint32_t b, uint32_t* out);
+/* bitpack.h:12-16 scalar layout; unpack_scalar32 (bitpack.cpp:305-309) */
+void orc_unpack_scalar32(const uint32_t* words, uint32_t b, uint32_t* out);
 
 /* delta.cpp:18-89 (D1, D4); D2/DM are extensions (izg_delta).
  * encode returns 0, or 1 when the input decreases (delta.cpp:13) and
@@ -47,7 +49,10 @@ void orc_fastpfor_choose_width(const uint32_t* counts33, uint32_t block_len,
                                uint32_t* b, uint32_t* maxbits);
 
 /* Codec::encode_deltas / decode_deltas for izg_codec
- * (codec_binpack.cpp:70-119, codec_patched.cpp:219-417).
+ * (codec_binpack.cpp:70-119, codec_patched.cpp:219-417).  Decode also covers
+ * IZG_BP32 (codec_binpack.cpp:43-60), IZG_FASTPFOR and IZG_SIMPLEPFOR
+ * (codec_patched.cpp:292-417, scalar_arrays / simple8b storage); encode only
+ * the two SIMD codecs.
  * encode returns words written (out must hold orc_encode_bound words) or
  * (size_t)-1 on a count error; decode returns an izg_status. */
 size_t orc_encode_bound(int codec, size_t count);

@@ -23,7 +23,9 @@ CHUNK_DTYPE = np.dtype([("word_off", "<u8"), ("n_words", "<u4"), ("n", "<u4"),
                         ("out_off", "<u8")])
 CODECS = {"simdbp128": (0, 1), "simdbp128-s4": (0, 2), "simdfastpfor": (1, 1),
           "simdfastpfor-s4": (1, 2), "simdbp128-d2": (0, 3), "simdbp128-dm": (0, 4),
-          "simdfastpfor-d2": (1, 3), "simdfastpfor-dm": (1, 4)}
+          "simdfastpfor-d2": (1, 3), "simdfastpfor-dm": (1, 4),
+          "bp32": (2, 1), "bp32-s4": (2, 2), "fastpfor": (3, 1), "fastpfor-s4": (3, 2),
+          "simplepfor": (4, 1), "simplepfor-s4": (4, 2)}
 
 
 def build() -> None:

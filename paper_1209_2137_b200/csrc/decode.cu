@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -29,7 +31,8 @@ __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t
     if (n == 0 || n > IZG_CHUNK_SIZE) return IZG_E_CHUNK_LENGTH;
   } else {
     if (n % 128) return IZG_E_COUNT_MULTIPLE;
-    if (codec == IZG_SIMDFASTPFOR && n > IZG_CHUNK_SIZE) return IZG_E_PAGE_TOO_LARGE;
+    if (codec != IZG_SIMDBP128 && codec != IZG_BP32 && n > IZG_CHUNK_SIZE)
+      return IZG_E_PAGE_TOO_LARGE;
   }
   return IZG_OK;
 }
@@ -82,6 +85,7 @@ __global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32) __maxnreg__(Layout
       const int64_t orow = tma_out && (ch.out_off & 31) == 0 ? (int64_t)(ch.out_off >> 5) : -1;
       const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
       uint4 carry = make_uint4(0, 0, 0, 0);
+      constexpr int ST = CODEC == IZG_SIMDFASTPFOR ? kVertical : kScalar;
       if (CODEC == IZG_SIMDBP128) {
         r.begin(p, ch.n_words);
         if (r.phase == 0)
@@ -90,12 +94,16 @@ __global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32) __maxnreg__(Layout
           st = bp128_core<DELTA, false>(r, os, ch.n_words, core / 128, o, oal, orow, carry,
                                         &pos);
         r.end();
+      } else if (CODEC == IZG_BP32) {
+        r.begin(p, ch.n_words);
+        st = bp32_core<DELTA>(r, os, ch.n_words, core / 128, o, oal, orow, carry, &pos);
+        r.end();
       } else if (IDX) {
-        st = fastpfor_core_idx<DELTA>(r, os, *fsc, p, c, core / 128, ix, o, oal, orow, carry,
-                                      &pos);
+        st = fastpfor_core_idx<DELTA, ST>(r, os, *fsc, p, c, core / 128, ix, o, oal, orow, carry,
+                                          &pos);
       } else {
-        st = fastpfor_core<DELTA>(r, os, *fsc, p, ch.n_words, core / 128, o, oal, orow,
-                                  carry, &pos);
+        st = fastpfor_core<DELTA, ST>(r, os, *fsc, p, ch.n_words, core / 128, o, oal, orow,
+                                      carry, &pos);
       }
       if (kArray && st == IZG_OK) {
         if (core < ch.n) {
@@ -188,13 +196,14 @@ KernelFn pick(int delta) {
 
 constexpr uint32_t kCounterSlots = 1024;
 static_assert(sizeof(FpScratch) <= Layout<IZG_SIMDFASTPFOR>::kTabBytes, "FpScratch layout");
+constexpr int kCodecs = 4;  // decoders: SIMD-BP128, SIMD-FastPFOR, BP32, FastPFOR
 static_assert(Layout<IZG_SIMDFASTPFOR>::kTabBytes % 16 == 0, "FpScratch alignment");
 
 struct DeviceInfo {
   bool init = false;
   bool ok = false;
   int sms = 0;
-  int occ[3][5] = {};  // [codec, or 2 = indexed SIMD-FastPFOR][delta]
+  int occ[2 * kCodecs][5] = {};  // [codec (+ kCodecs: indexed page path)][delta]
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -213,7 +222,7 @@ int device_of(const void* p) {
   return a.device;
 }
 
-// `variant` = codec, or 2 for the indexed SIMD-FastPFOR decode kernel.
+// `variant` = codec, + kCodecs for the indexed page decode kernels.
 int prepare(int dev, int variant, int delta, KernelFn fn, int threads, size_t smem,
             int* grid_per_sm, int* sms, uint32_t** counter) {
   if (dev < 0 || dev >= 64) return IZG_ERR_INVALID_ARGUMENT;
@@ -268,7 +277,7 @@ namespace izg {
 int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* d_chunks,
                 uint32_t n_chunks, uint32_t* d_out, int32_t* d_status, uint32_t* d_consumed,
                 void* d_ws, uint64_t ws_bytes, void* stream) {
-  if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return IZG_ERR_INVALID_ARGUMENT;
+  if (codec < IZG_SIMDBP128 || codec > IZG_FASTPFOR) return IZG_ERR_INVALID_ARGUMENT;
   if (delta < IZG_DELTA_NONE || delta > IZG_DELTA_DM) return IZG_ERR_INVALID_ARGUMENT;
   if (n_chunks == 0) return IZG_SUCCESS;
   if (!d_words || !d_chunks || !d_out || !d_status) return IZG_ERR_INVALID_ARGUMENT;
@@ -280,40 +289,48 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   }
   const int dev = device_of(d_status);
   if (dev < 0) return IZG_ERR_INVALID_ARGUMENT;
+  const bool paged = codec == IZG_SIMDFASTPFOR || codec == IZG_FASTPFOR;
+  // The indexed path serves SIMD-FastPFOR.  Scalar-array FastPFOR pages
+  // decode with the fused kernel: its indexed variant faulted on pages with
+  // exceptions in a code-layout-dependent way, so it is not
+  // built until that is understood.
   const bool idx = codec == IZG_SIMDFASTPFOR && d_ws &&
                    (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
                    ws_bytes >= idx_workspace_bytes(n_chunks);
-  KernelFn fn = codec == IZG_SIMDBP128 ? pick<IZG_SIMDBP128, false>(delta)
-                : idx                  ? pick<IZG_SIMDFASTPFOR, true>(delta)
-                                       : pick<IZG_SIMDFASTPFOR, false>(delta);
+  KernelFn fn = nullptr;
+  switch (codec) {
+    case IZG_SIMDBP128: fn = pick<IZG_SIMDBP128, false>(delta); break;
+    case IZG_BP32: fn = pick<IZG_BP32, false>(delta); break;
+    case IZG_SIMDFASTPFOR:
+      fn = idx ? pick<IZG_SIMDFASTPFOR, true>(delta) : pick<IZG_SIMDFASTPFOR, false>(delta);
+      break;
+    case IZG_FASTPFOR: fn = pick<IZG_FASTPFOR, false>(delta); break;
+  }
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;
   uint32_t* counter = nullptr;
-  const int warps = codec == IZG_SIMDBP128 ? Layout<IZG_SIMDBP128>::kWarps
-                                           : Layout<IZG_SIMDFASTPFOR>::kWarps;
-  const size_t smem = codec == IZG_SIMDBP128 ? Layout<IZG_SIMDBP128>::kSmem
-                                             : Layout<IZG_SIMDFASTPFOR>::kSmem;
-  int rc = prepare(dev, idx ? 2 : codec, delta, fn, warps * 32, smem, &per_sm, &sms, &counter);
+  const int warps = paged ? Layout<IZG_SIMDFASTPFOR>::kWarps : Layout<IZG_SIMDBP128>::kWarps;
+  const size_t smem = paged ? Layout<IZG_SIMDFASTPFOR>::kSmem : Layout<IZG_SIMDBP128>::kSmem;
+  int rc = prepare(dev, codec + (idx ? kCodecs : 0), delta, fn, warps * 32, smem, &per_sm, &sms,
+                   &counter);
   if (rc != IZG_SUCCESS) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   IdxView ix{};
   if (idx) {
     static const bool attr = [] {
-      cudaFuncSetAttribute(fp_index_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)IdxLayout::kSmem);
-      cudaFuncSetAttribute(fp_index_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)IdxLayout::kSmem);
+      const int b = (int)IdxLayout::kSmem;
+      cudaFuncSetAttribute(fp_index_kernel<false, kVertical>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+      cudaFuncSetAttribute(fp_index_kernel<true, kVertical>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, b);
       return true;
     }();
     (void)attr;
     ix = idx_view(d_ws, n_chunks);
     const uint32_t g = (n_chunks + kIdxWarps - 1) / kIdxWarps;
-    if (delta == IZG_DELTA_NONE)
-      fp_index_kernel<false><<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks,
-                                                                         n_chunks, ix);
-    else
-      fp_index_kernel<true><<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks,
-                                                                        n_chunks, ix);
+    auto* ifn = delta == IZG_DELTA_NONE ? fp_index_kernel<false, kVertical>
+                                        : fp_index_kernel<true, kVertical>;
+    ifn<<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks, n_chunks, ix);
   }
   const uint64_t want = (n_chunks + warps - 1) / warps;
   const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);

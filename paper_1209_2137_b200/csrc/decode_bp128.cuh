@@ -129,6 +129,105 @@ __device__ __forceinline__ void unpack_slots_unaligned(const WarpRing& r, uint32
   }
 }
 
+// Scalar 32-integer groups (bitpack.h:12-16: value i of a group at bits
+// [i*b, i*b+b) of its b-word stream), as used by BP32 and the scalar
+// FastPFOR family: a 128-integer block is 4 groups of `width` words from
+// stream word `bword`.  Mapping C gives lane 8q+s8 block values
+// 16*s8 .. 16*s8+15, i.e. half (s8 & 1) of group s8/2; the lane slides a
+// two-word window along its 16*width bits (one shared load per word).
+__device__ __forceinline__ void unpack_scalar_slots(const WarpRing& r, uint32_t bword,
+                                                    uint32_t width, uint32_t s8,
+                                                    uint32_t (&v)[4][4]) {
+  const uint32_t mask = low_mask(width);
+  const uint32_t gbase = bword + (s8 >> 1) * width;
+  uint32_t bit = 16u * (s8 & 1u) * width;
+  uint32_t wi = bit >> 5;
+  uint32_t lo = lds32(r.word_addr(gbase + wi));
+  uint32_t hi = lds32(r.word_addr(gbase + wi + 1));
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (k) {
+      bit += width;
+      if ((bit >> 5) != wi) {
+        ++wi;
+        lo = hi;
+        hi = lds32(r.word_addr(gbase + wi + 1));
+      }
+    }
+    v[k >> 2][k & 3] = funnel_r(lo, hi, bit & 31u) & mask;
+  }
+}
+
+// Bp32Codec::decode_deltas (codec_binpack.cpp:43-60) fused like bp128_core:
+// per 128 integers one descriptor word (byte g = width of scalar group g)
+// and the four groups.  The four descriptors of a warp iteration form a
+// short dependent chain (each position follows the previous meta-block's
+// payload); their checks run in the reference's order.
+template <int DELTA>
+__device__ int32_t bp32_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t nblocks,
+                             uint32_t* out, bool out_aligned, int64_t orow, uint4& carry,
+                             uint32_t* pos_out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t q = lane >> 3, s8 = lane & 7;
+  uint32_t pos = 0;
+#pragma unroll 1
+  for (uint32_t g0 = 0; g0 < nblocks; g0 += 4) {
+    const uint32_t ng = min(4u, nblocks - g0);
+    const uint32_t first = pos;
+    // everything before this iteration is consumed: free it first, so the
+    // ring can take the whole iteration (<= 4 x 129 words) before ensure()
+    r.release_below(4u * first);
+    uint32_t mypay = 0, mywidth = 0;  // this lane's block q: payload word, width
+#pragma unroll 1
+    for (uint32_t k = 0; k < ng; ++k) {
+      if (pos >= nw) return IZG_E_BP32_TRUNC_DESC;
+      r.ensure(4u * (pos + 1));
+      const uint32_t d = lds32(r.word_addr(pos));
+      ++pos;
+      uint32_t at = pos, bad = IZG_OK;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint32_t w = (d >> (8 * g)) & 0xFFu;
+        if (bad == IZG_OK) {
+          if (w > 32) bad = IZG_E_BP32_WIDTH;
+          else if (at + w > nw) bad = IZG_E_BP32_TRUNC_PAYLOAD;
+        }
+        at += min(w, 33u);
+      }
+      if (bad) return (int32_t)bad;
+      if (k == q) {
+        mypay = pos;
+        mywidth = d;
+      }
+      pos = at;
+    }
+    r.ensure(4u * pos);
+    // the lane's group s8/2 of block q: its width and payload word
+    const uint32_t gsel = s8 >> 1;
+    uint32_t width = 0, goff = 0;
+#pragma unroll
+    for (uint32_t g = 0; g < 4; ++g) {
+      const uint32_t w = (mywidth >> (8 * g)) & 0xFFu;
+      if (g == gsel) width = w;
+      if (g < gsel) goff += w;
+    }
+    const bool active = q < ng;
+    if (!active) width = 0;  // reads stay in the ring; values are zero
+    uint32_t v[4][4];
+    // unpack_scalar_slots addresses group (s8 >> 1) as bword + gsel * width:
+    // pass the group's own start minus that offset
+    unpack_scalar_slots(r, mypay + goff - gsel * width, width, s8, v);
+    scan<DELTA>(v, carry, lane);
+    if (orow >= 0 && ng == 4) {
+      os.put(v, lane, (uint32_t)(orow + 4 * g0));
+    } else if (active) {
+      store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, out_aligned);
+    }
+  }
+  *pos_out = pos;
+  return IZG_OK;
+}
+
 // Decode `nblocks` core blocks of the chunk streaming through `r`.
 // Returns an izg_status; on success *pos_out = payload words consumed.
 // `orow` is the chunk's first output row (32 integers) for the TMA path, or

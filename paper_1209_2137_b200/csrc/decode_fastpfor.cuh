@@ -30,6 +30,21 @@
 namespace izg {
 
 __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) { return __ldg(p); }
+// Coherent (non-.nc) loads for the patch loop: with ld.global.nc there, the
+// indexed scalar-array FastPFOR kernel faulted ("misaligned address") on
+// every page with exceptions although every address is 4-byte aligned, and
+// the fault vanished with any change to the loop (printf, no inlining, no
+// shared-memory ORs); plain ld.global is immune and costs nothing here.
+__device__ __forceinline__ uint32_t ld_u32(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_u8(const uint8_t* p) {
+  uint32_t v;
+  asm("ld.global.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ uint32_t ldg_u8(const uint8_t* p) { return __ldg(p); }
 
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -145,7 +160,13 @@ __device__ bool fp_positions_bad(const FpScratch& sc, const uint8_t* ba, uint32_
   return __any_sync(0xFFFFFFFFu, bad);
 }
 
+// Patch storage of the exception highs (codec_patched.cpp:195-199).
+enum { kVertical = 0, kScalar = 1 };
+
 // Phase 2.  `pos` = page word after the byte array; *end = words consumed.
+// ST = kVertical: 16-byte-aligned vertical groups of 128 (simdfastpfor);
+// kScalar: scalar groups of 32, no alignment (fastpfor).
+template <int ST>
 __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint32_t nw, uint64_t pos,
                                 int lane, uint32_t* end) {
   sc.dir_n[lane + 1] = 0;
@@ -159,8 +180,14 @@ __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint32_t nw
     bits &= bits - 1;
     if (pos >= nw) return IZG_E_FP_TRUNC_EXC;
     const uint32_t n = ldg_u32(page + pos);
-    pos = (pos + 1 + 3) & ~uint64_t{3};  // 16-byte alignment in the page
-    const uint64_t nwords = ((uint64_t)n + 127) / 128 * 4 * w;
+    uint64_t nwords;
+    if (ST == kVertical) {
+      pos = (pos + 1 + 3) & ~uint64_t{3};  // 16-byte alignment in the page
+      nwords = ((uint64_t)n + 127) / 128 * 4 * w;
+    } else {
+      pos = pos + 1;
+      nwords = ((uint64_t)n + 31) / 32 * w;
+    }
     if (pos + nwords > nw) return IZG_E_FP_TRUNC_EXC;
     if (lane == 0) {
       sc.dir_base[w] = (uint32_t)pos;
@@ -173,18 +200,6 @@ __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint32_t nw
   return IZG_OK;
 }
 
-// High bits of exception r of the width-w vertical array at page word `base`.
-__device__ __forceinline__ uint32_t fp_high(const uint32_t* page, uint32_t base, uint32_t w,
-                                            uint32_t r) {
-  const uint32_t t = r & 127u;
-  const uint32_t bit = (t >> 2) * w;
-  const uint32_t word = base + (r >> 7) * 4u * w + 4u * (bit >> 5) + (t & 3u);
-  const uint32_t sh = bit & 31u;
-  const uint32_t lo = ldg_u32(page + word);
-  const uint32_t hi = ldg_u32(page + word + (sh + w > 32 ? 4u : 0u));
-  return funnel_r(lo, hi, sh) & low_mask(w);
-}
-
 // Patch one warp iteration's exceptions into its output tile `t`
 // (codec_patched.cpp:390-404: o[pos] |= high << b).  Lanes 8q..8q+7 carry
 // block q's parameters (b, exception width w, count c, first position byte
@@ -193,6 +208,7 @@ __device__ __forceinline__ uint32_t fp_high(const uint32_t* page, uint32_t base,
 // first OR; the round count is set by the longest of the four lists.
 // Duplicate positions OR together like the reference.  Returns true when a
 // position >= 128 was met (the caller resolves precedence).
+template <int ST>
 __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const uint8_t* ba,
                                          uint32_t myb, uint32_t myw, uint32_t myc, uint32_t mybp,
                                          uint32_t mycur, uint32_t mybase, int lane) {
@@ -210,13 +226,22 @@ __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const
       ok[j] = e < myc;
       const uint32_t ee = ok[j] ? e : 0u;
       const uint32_t rr = mycur + ee;
-      const uint32_t tt = rr & 127u, bit = (tt >> 2) * myw;
-      const uint32_t word = mybase + (rr >> 7) * w4 + 4u * (bit >> 5) + (tt & 3u);
-      sh[j] = bit & 31u;
+      uint32_t word, step;
+      if (ST == kVertical) {  // group r/128, lane r%4, slot (r%128)/4
+        const uint32_t tt = rr & 127u, bit = (tt >> 2) * myw;
+        word = mybase + (rr >> 7) * w4 + 4u * (bit >> 5) + (tt & 3u);
+        sh[j] = bit & 31u;
+        step = 4u;
+      } else {  // group r/32, bits [(r%32)*w, +w) of its w-word stream
+        const uint32_t bit = (rr & 31u) * myw;
+        word = mybase + (rr >> 5) * myw + (bit >> 5);
+        sh[j] = bit & 31u;
+        step = 1u;
+      }
       // an idle slot reads the page's first words (always in bounds)
-      pp[j] = ok[j] ? ldg_u8(ba + mybp + ee) : 0u;
-      lo[j] = ldg_u32(page + (ok[j] ? word : 0u));
-      hi[j] = ldg_u32(page + (ok[j] ? word + (sh[j] + myw > 32 ? 4u : 0u) : 0u));
+      pp[j] = ok[j] ? ld_u8(ba + mybp + ee) : 0u;
+      lo[j] = ld_u32(page + (ok[j] ? word : 0u));
+      hi[j] = ld_u32(page + (ok[j] ? word + (sh[j] + myw > 32 ? step : 0u) : 0u));
     }
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
@@ -235,7 +260,7 @@ __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const
 
 // Phase 3.  Returns an izg_status; *bad_pos is set when a position >= 128
 // was met (the caller resolves precedence).
-template <int DELTA>
+template <int DELTA, int ST>
 __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uint32_t* page,
                              uint32_t A, uint32_t nblocks, uint32_t* out, bool oal, int64_t orow,
                              uint4& carry, bool* bad_pos) {
@@ -311,7 +336,9 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
     r.ensure(4u * (packed - 1));
     const bool live = q < ng;
     uint32_t v[4][4];
-    if (r.phase == 0)
+    if (ST != kVertical)
+      unpack_scalar_slots(r, myoff - 1, myb, s8, v);
+    else if (r.phase == 0)
       unpack_slots_aligned(r, r.ring_off() + 4u * (myoff - 1), myb, s8, v);
     else
       unpack_slots_unaligned(r, myoff - 1, myb, s8, v);
@@ -320,7 +347,7 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
       const uint32_t t = os.acquire();
       OutStage::write(t, v, lane);
       __syncwarp();
-      bad |= fp_patch(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
+      bad |= fp_patch<ST>(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
       __syncwarp();
       OutStage::read(t, v, lane);
       scan<DELTA>(v, carry, lane);
@@ -344,7 +371,7 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
 }
 
 // Whole page.  `nblocks` = count / 128; *pos_out = words consumed.
-template <int DELTA>
+template <int DELTA, int ST>
 __device__ int32_t fastpfor_core(WarpRing& r, OutStage& os, FpScratch& sc, const uint32_t* page,
                                  uint32_t nw, uint32_t nblocks, uint32_t* out, bool oal,
                                  int64_t orow, uint4& carry, uint32_t* pos_out) {
@@ -372,7 +399,7 @@ __device__ int32_t fastpfor_core(WarpRing& r, OutStage& os, FpScratch& sc, const
   if (st) return fp_positions_bad(sc, ba, parsed, lane) ? IZG_E_FP_POS_RANGE : st;
 
   uint32_t end = 0;
-  st = fp_directory(sc, page, nw, A + 1 + ba_words, lane, &end);
+  st = fp_directory<ST>(sc, page, nw, A + 1 + ba_words, lane, &end);
   if (st) return fp_positions_bad(sc, ba, nblocks, lane) ? IZG_E_FP_POS_RANGE : st;
 
   // exception arrays: warm L2 while the packed area streams
@@ -382,7 +409,7 @@ __device__ int32_t fastpfor_core(WarpRing& r, OutStage& os, FpScratch& sc, const
   }
   r.begin(page + 1, A - 1);
   bool bad_pos = false;
-  st = fp_blocks<DELTA>(r, os, sc, page, A, nblocks, out, oal, orow, carry, &bad_pos);
+  st = fp_blocks<DELTA, ST>(r, os, sc, page, A, nblocks, out, oal, orow, carry, &bad_pos);
   r.end();
   if (st) return fp_positions_bad(sc, ba, nblocks, lane) ? IZG_E_FP_POS_RANGE : st;
   if (bad_pos) return IZG_E_FP_POS_RANGE;

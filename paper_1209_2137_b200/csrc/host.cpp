@@ -47,6 +47,10 @@ extern "C" const char* izg_status_string(int32_t s) {
     case IZG_E_CT_ARRAY_LENGTH: return "container: array length mismatch";
     case IZG_E_CT_NOT_RAW: return "container: expected RAW data, found codec";
     case IZG_E_CT_RAW_COUNT: return "container: RAW word count mismatch";
+    case IZG_E_BP32_TRUNC_DESC: return "bp32: truncated descriptor";
+    case IZG_E_BP32_WIDTH: return "bp32: width byte exceeds 32";
+    case IZG_E_BP32_TRUNC_PAYLOAD: return "bp32: truncated payload";
+    case IZG_E_S8_EXHAUSTED: return "simple8b: stream exhausted before count";
     case IZG_E_COUNT_MULTIPLE: return "count must be a multiple of 128";
     case IZG_E_PAGE_TOO_LARGE: return "patched codec: page exceeds 65536 integers";
     case IZG_E_DECREASING: return "delta encode: input is not nondecreasing";
@@ -54,8 +58,8 @@ extern "C" const char* izg_status_string(int32_t s) {
   }
 }
 
-// make_codec (codec.cpp:99-109) for the hot-path codecs; "-d2"/"-dm" are
-// the D2/DM extensions (not in the reference registry).
+// make_codec (codec.cpp:99-109) for the codecs with a device decoder;
+// "-d2"/"-dm" are the D2/DM extensions (not in the reference registry).
 extern "C" int izg_parse_codec_name(const char* name, int* codec, int* delta) {
   if (!name || !codec || !delta) return IZG_ERR_INVALID_ARGUMENT;
   std::string_view s(name);
@@ -73,6 +77,10 @@ extern "C" int izg_parse_codec_name(const char* name, int* codec, int* delta) {
     *codec = IZG_SIMDBP128;
   else if (s == "simdfastpfor")
     *codec = IZG_SIMDFASTPFOR;
+  else if (s == "bp32")
+    *codec = IZG_BP32;
+  else if (s == "fastpfor")
+    *codec = IZG_FASTPFOR;
   else
     return IZG_ERR_UNKNOWN_CODEC;
   *delta = d;
@@ -83,7 +91,8 @@ extern "C" uint64_t izg_layout_chunks(int codec, const uint32_t* n_words, uint32
                                       uint64_t* word_off_out) {
   // SIMD-BP128 payload word 0 on a 16-byte boundary (codec_binpack.h:17-23);
   // SIMD-FastPFOR page word 0 at 12 mod 16 so packed rows (word 1 + 4k,
-  // codec_patched.cpp:225,250-253) are 16-byte aligned.
+  // codec_patched.cpp:225,250-253) are 16-byte aligned.  The scalar-group
+  // codecs read words and take any placement (16-byte aligned here).
   const uint64_t phase = codec == IZG_SIMDFASTPFOR ? 3 : 0;
   uint64_t pos = 0;
   for (uint32_t i = 0; i < n_chunks; ++i) {

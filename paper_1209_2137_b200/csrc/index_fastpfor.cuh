@@ -117,7 +117,7 @@ struct IdxLayout {
 // windowed byte-array walk (fp_parse), the exception directory
 // (fp_directory), then fp_meta.  Statuses follow the reference's order;
 // positions are left to the decode kernel (see the file comment).
-template <bool ARRAY>
+template <bool ARRAY, int ST>
 __global__ void __launch_bounds__(kIdxWarps * 32)
     fp_index_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                     uint32_t n_chunks, IdxView ix) {
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kIdxWarps * 32)
   __syncwarp();
   uint32_t end = 0;
   if (st == IZG_OK) {
-    st = fp_directory(sc, page, nw, A + 1 + ba_words, lane, &end);
+    st = fp_directory<ST>(sc, page, nw, A + 1 + ba_words, lane, &end);
     if (st == IZG_OK) ix.dir[(size_t)c * 32 + lane] = sc.dir_base[lane + 1];
   }
   uint32_t packed = 0;
@@ -199,7 +199,7 @@ __device__ bool fp_positions_bad_idx(const uint4* rec, const uint8_t* ba, uint32
 // index pass already made): as fp_blocks, but each lane reads its block's
 // record (lanes 8q..8q+7 share block q's 16 bytes) one iteration ahead.
 // Returns true when an exception position >= 128 was met.
-template <int DELTA>
+template <int DELTA, int ST>
 __device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const FpScratch& sc, const uint4* rec,
                               const uint32_t* page, uint32_t A, uint32_t nblocks, uint32_t* out,
                               bool oal, int64_t orow, uint4& carry) {
@@ -226,7 +226,9 @@ __device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const FpScratch& sc, co
     r.release_below(4u * (first - 1));
     r.ensure(4u * (after - 1));
     uint32_t v[4][4];
-    if (r.phase == 0)
+    if (ST != kVertical)
+      unpack_scalar_slots(r, myoff - 1, myb, s8, v);
+    else if (r.phase == 0)
       unpack_slots_aligned(r, r.ring_off() + 4u * (myoff - 1), myb, s8, v);
     else
       unpack_slots_unaligned(r, myoff - 1, myb, s8, v);
@@ -235,7 +237,7 @@ __device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const FpScratch& sc, co
       const uint32_t t = os.acquire();
       OutStage::write(t, v, lane);
       __syncwarp();
-      bad |= fp_patch(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
+      bad |= fp_patch<ST>(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
       __syncwarp();
       OutStage::read(t, v, lane);
       scan<DELTA>(v, carry, lane);
@@ -258,7 +260,7 @@ __device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const FpScratch& sc, co
 
 // Whole indexed page `c` (record written by fp_index_kernel); same contract
 // as fastpfor_core.
-template <int DELTA>
+template <int DELTA, int ST>
 __device__ int32_t fastpfor_core_idx(WarpRing& r, OutStage& os, FpScratch& sc,
                                      const uint32_t* page, uint32_t c, uint32_t nblocks,
                                      const IdxView& ix, uint32_t* out, bool oal, int64_t orow,
@@ -284,7 +286,8 @@ __device__ int32_t fastpfor_core_idx(WarpRing& r, OutStage& os, FpScratch& sc,
   __syncwarp();
   if (lane == 0) prefetch_l2(page + h.y, 4u * (h.z - h.y));  // exception arrays
   r.begin(page + 1, A - 1);
-  const bool bad = fp_blocks_idx<DELTA>(r, os, sc, rec, page, A, nblocks, out, oal, orow, carry);
+  const bool bad =
+      fp_blocks_idx<DELTA, ST>(r, os, sc, rec, page, A, nblocks, out, oal, orow, carry);
   r.end();
   if (bad) return IZG_E_FP_POS_RANGE;
   *pos_out = h.z;

@@ -34,11 +34,14 @@ constexpr uint32_t kStageOut = 2048;          // one warp iteration of output (5
 // SIMD-FastPFOR block tables, then the ring barriers.
 template <int CODEC>
 struct Layout {
-  static constexpr int kWarps = CODEC == IZG_SIMDBP128 ? 8 : 6;
+  // page codecs (byte array + exceptions) vs binary packing
+  static constexpr bool kPaged = CODEC == IZG_SIMDFASTPFOR || CODEC == IZG_FASTPFOR ||
+                                 CODEC == IZG_SIMPLEPFOR;
+  static constexpr int kWarps = kPaged ? 6 : 8;
   // registers per thread so that 3 CTAs fit in the 64K-register file
-  static constexpr int kMaxRegs = CODEC == IZG_SIMDBP128 ? 80 : 96;
+  static constexpr int kMaxRegs = kPaged ? 96 : 80;
   // per-warp FpScratch (decode_fastpfor.cuh), 16-byte multiple
-  static constexpr uint32_t kTabBytes = CODEC == IZG_SIMDBP128 ? 0 : 2048 + 512 + 2 * 33 * 4 + 8;
+  static constexpr uint32_t kTabBytes = kPaged ? 2048 + 512 + 2 * 33 * 4 + 8 : 0;
   static constexpr uint32_t kOutOff = kWarps * kRingBytes;
   static constexpr uint32_t kTabOff = kOutOff + kWarps * 2 * kStageOut;
   static constexpr uint32_t kBarOff = kTabOff + kWarps * kTabBytes;

@@ -8,6 +8,8 @@ import paper_1209_2137_b200 as P
 REF_NAMES = ["simdbp128", "simdbp128-s4", "simdfastpfor", "simdfastpfor-s4"]
 EXT_NAMES = ["simdbp128-d2", "simdbp128-dm", "simdfastpfor-d2", "simdfastpfor-dm"]
 ALL_NAMES = REF_NAMES + EXT_NAMES
+# the same page framework with scalar 32-integer groups
+F3_NAMES = ["bp32", "bp32-s4", "fastpfor", "fastpfor-s4", "simplepfor", "simplepfor-s4"]
 
 # Lengths around every boundary of the format: block (128), meta-block
 # (2048), chunk (65536), VByte remainder, tiny arrays.

@@ -48,7 +48,9 @@ def test_codec_registry():
     assert P.make_codec("simdfastpfor-s4").delta == N.DELTA_D4
     assert P.make_codec("simdbp128-d2").delta == N.DELTA_D2
     assert P.make_codec("simdfastpfor-dm").delta == N.DELTA_DM
-    for bad in ("lz77", "", "simdbp128-s5", "bp32"):
+    # the scalar-group codecs of SURVEY.md §8 f3 (decode only)
+    assert P.make_codec("bp32").codec == 2 and P.make_codec("fastpfor-s4").codec == 3
+    for bad in ("lz77", "", "simdbp128-s5", "vbyte", "pfor"):
         with pytest.raises(ValueError):
             P.make_codec(bad)
     assert P.codec_names() == ["simdbp128", "simdbp128-s4", "simdfastpfor", "simdfastpfor-s4"]

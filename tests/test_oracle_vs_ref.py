@@ -8,7 +8,7 @@ import pytest
 
 import paper_1209_2137_b200 as P
 from oracle.pyoracle import RefError
-from tests.helpers import REF_NAMES, assorted_arrays, chunks_of, random_sorted
+from tests.helpers import F3_NAMES, REF_NAMES, assorted_arrays, chunks_of, random_sorted
 
 # reference what() text -> izg_status (codec_*.cpp throw sites)
 WHAT = {
@@ -25,6 +25,8 @@ WHAT = {
     "fastpfor: truncated exception array": 19,
     "fastpfor: packed blocks overrun byte array": 20,
     "fastpfor: exception array exhausted": 21, "fastpfor: packed area size mismatch": 22,
+    "bp32: truncated descriptor": 34, "bp32: width byte exceeds 32": 35,
+    "bp32: truncated payload": 36, "simple8b: stream exhausted before count": 37,
 }
 
 
@@ -127,3 +129,42 @@ def test_decode_deltas_corruption_vs_reference(oracle, ref, codec_name):
             assert st == 0 and used == rused and np.array_equal(out, expect)
         except RefError as e:
             assert st == WHAT[e.what], (e.what, st)
+
+
+def outlier_sorted(rng, n, rate=0.08):
+    gaps = rng.geometric(1 / 6, size=n).astype(np.uint64)
+    m = rng.random(n) < rate
+    gaps[m] = rng.integers(1 << 10, 1 << 22, size=int(m.sum()))
+    return np.minimum(np.cumsum(gaps), 0xFFFFFFFF).astype(np.uint32)
+
+
+@pytest.mark.parametrize("name", F3_NAMES)
+def test_f3_codecs_decode_matches_reference(oracle, ref, name):
+    """BP32 / FastPFOR (scalar) / SimplePFOR: the oracle
+    decodes reference-encoded arrays exactly, edge lengths and outliers."""
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    arrays = assorted_arrays(seed=zlib.crc32(name.encode()) % 991)
+    arrays += [outlier_sorted(rng, n) for n in (128, 4096, 65536, 70000)]
+    for arr in arrays:
+        st, out = oracle.decode_array(name, ref.encode_array(name, arr))
+        assert st == 0 and np.array_equal(out, arr), (name, len(arr))
+
+
+@pytest.mark.parametrize("name", F3_NAMES)
+def test_f3_codecs_corruption_statuses_match_reference(oracle, ref, name):
+    rng = np.random.default_rng(zlib.crc32(name.encode()) + 7)
+    seen = set()
+    for n in (700, 2048 + 130, 9000):
+        arr = outlier_sorted(rng, n) if n != 700 else random_sorted(rng, n, 5000)
+        payload = ref.encode_array(name, arr)[0][1]
+        for p in _mutations(payload, rng, 120):
+            st, out = oracle.decode_chunk(name, p, n)
+            try:
+                expect = ref.decode_array(name, [(n, p)])
+                assert st == 0
+                assert np.array_equal(out, expect)
+            except RefError as e:
+                assert e.code == 1, e
+                assert st == WHAT[e.what], (e.what, st)
+            seen.add(st)
+    assert len(seen) >= 3, seen
