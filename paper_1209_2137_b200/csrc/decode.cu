@@ -42,13 +42,14 @@ __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t
 // VByte remainder, consumption check, status.  IDX (SIMD-FastPFOR only):
 // pages were indexed by fp_index_kernel into `ix`.
 template <int CODEC, int DELTA, bool IDX>
-__global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32) __maxnreg__(Layout<CODEC>::kMaxRegs)
+__global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
+    __maxnreg__((Layout<CODEC, IDX>::kMaxRegs))
     decode_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                   uint32_t n_chunks, uint32_t* __restrict__ out, int32_t* __restrict__ status,
                   uint32_t* __restrict__ consumed, uint32_t* __restrict__ next_chunk,
                   const __grid_constant__ CUtensorMap omap, int tma_out, IdxView ix) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  using LY = Layout<CODEC>;
+  using LY = Layout<CODEC, IDX>;
   constexpr bool kArray = DELTA != IZG_DELTA_NONE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRing r;
@@ -99,8 +100,8 @@ __global__ void __launch_bounds__(Layout<CODEC>::kWarps * 32) __maxnreg__(Layout
         st = bp32_core<DELTA>(r, os, ch.n_words, core / 128, o, oal, orow, carry, &pos);
         r.end();
       } else if (IDX) {
-        st = fastpfor_core_idx<DELTA, ST>(r, os, *fsc, p, c, core / 128, ix, o, oal, orow, carry,
-                                          &pos);
+        st = fastpfor_core_idx<DELTA, ST>(r, os, reinterpret_cast<uint32_t*>(fsc), p, c,
+                                          core / 128, ix, o, oal, orow, carry, &pos);
       } else {
         st = fastpfor_core<DELTA, ST>(r, os, *fsc, p, ch.n_words, core / 128, o, oal, orow,
                                       carry, &pos);
@@ -310,7 +311,9 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   int per_sm = 0, sms = 0;
   uint32_t* counter = nullptr;
   const int warps = paged ? Layout<IZG_SIMDFASTPFOR>::kWarps : Layout<IZG_SIMDBP128>::kWarps;
-  const size_t smem = paged ? Layout<IZG_SIMDFASTPFOR>::kSmem : Layout<IZG_SIMDBP128>::kSmem;
+  const size_t smem = idx     ? Layout<IZG_SIMDFASTPFOR, true>::kSmem
+                      : paged ? Layout<IZG_SIMDFASTPFOR>::kSmem
+                              : Layout<IZG_SIMDBP128>::kSmem;
   int rc = prepare(dev, codec + (idx ? kCodecs : 0), delta, fn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;

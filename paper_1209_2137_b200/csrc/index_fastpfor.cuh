@@ -200,7 +200,7 @@ __device__ bool fp_positions_bad_idx(const uint4* rec, const uint8_t* ba, uint32
 // record (lanes 8q..8q+7 share block q's 16 bytes) one iteration ahead.
 // Returns true when an exception position >= 128 was met.
 template <int DELTA, int ST>
-__device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const FpScratch& sc, const uint4* rec,
+__device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const uint32_t* dir_base, const uint4* rec,
                               const uint32_t* page, uint32_t A, uint32_t nblocks, uint32_t* out,
                               bool oal, int64_t orow, uint4& carry) {
   const int lane = threadIdx.x & 31;
@@ -233,7 +233,7 @@ __device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const FpScratch& sc, co
     else
       unpack_slots_unaligned(r, myoff - 1, myb, s8, v);
     if (tot) {
-      const uint32_t mybase = sc.dir_base[myw];
+      const uint32_t mybase = dir_base[myw];
       const uint32_t t = os.acquire();
       OutStage::write(t, v, lane);
       __syncwarp();
@@ -261,7 +261,7 @@ __device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const FpScratch& sc, co
 // Whole indexed page `c` (record written by fp_index_kernel); same contract
 // as fastpfor_core.
 template <int DELTA, int ST>
-__device__ int32_t fastpfor_core_idx(WarpRing& r, OutStage& os, FpScratch& sc,
+__device__ int32_t fastpfor_core_idx(WarpRing& r, OutStage& os, uint32_t* dir_base,
                                      const uint32_t* page, uint32_t c, uint32_t nblocks,
                                      const IdxView& ix, uint32_t* out, bool oal, int64_t orow,
                                      uint4& carry, uint32_t* pos_out) {
@@ -282,12 +282,12 @@ __device__ int32_t fastpfor_core_idx(WarpRing& r, OutStage& os, FpScratch& sc,
                : st;
   }
   const uint32_t A = h.w;
-  sc.dir_base[lane + 1] = ix.dir[(size_t)c * 32 + lane];
+  dir_base[lane + 1] = ix.dir[(size_t)c * 32 + lane];
   __syncwarp();
   if (lane == 0) prefetch_l2(page + h.y, 4u * (h.z - h.y));  // exception arrays
   r.begin(page + 1, A - 1);
   const bool bad =
-      fp_blocks_idx<DELTA, ST>(r, os, sc, rec, page, A, nblocks, out, oal, orow, carry);
+      fp_blocks_idx<DELTA, ST>(r, os, dir_base, rec, page, A, nblocks, out, oal, orow, carry);
   r.end();
   if (bad) return IZG_E_FP_POS_RANGE;
   *pos_out = h.z;

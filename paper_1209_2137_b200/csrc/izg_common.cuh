@@ -32,16 +32,24 @@ constexpr uint32_t kStageOut = 2048;          // one warp iteration of output (5
 // Shared memory per CTA: the warps' rings, then 2 output staging tiles per
 // warp (1024-byte aligned for the 128-byte TMA swizzle), then per-warp
 // SIMD-FastPFOR block tables, then the ring barriers.
-template <int CODEC>
+template <int CODEC, bool IDX = false>
 struct Layout {
   // page codecs (byte array + exceptions) vs binary packing
   static constexpr bool kPaged = CODEC == IZG_SIMDFASTPFOR || CODEC == IZG_FASTPFOR ||
                                  CODEC == IZG_SIMPLEPFOR;
   static constexpr int kWarps = kPaged ? 6 : 8;
-  // registers per thread so that 3 CTAs fit in the 64K-register file
-  static constexpr int kMaxRegs = kPaged ? 96 : 80;
-  // per-warp FpScratch (decode_fastpfor.cuh), 16-byte multiple
-  static constexpr uint32_t kTabBytes = kPaged ? 2048 + 512 + 2 * 33 * 4 + 8 : 0;
+  // registers per thread: 3 CTAs per SM for the fused kernels; the indexed
+  // page decode (no parse or metadata state) fits 4 CTAs of 6 warps
+#ifndef IZG_PAGED_MAXREGS
+#define IZG_PAGED_MAXREGS 96
+#endif
+#ifndef IZG_IDX_MAXREGS
+#define IZG_IDX_MAXREGS 80
+#endif
+  static constexpr int kMaxRegs = !kPaged ? 80 : IDX ? IZG_IDX_MAXREGS : IZG_PAGED_MAXREGS;
+  // per-warp scratch, 16-byte multiple: the fused page kernels' FpScratch
+  // (decode_fastpfor.cuh), the indexed one's exception directory only
+  static constexpr uint32_t kTabBytes = !kPaged ? 0 : IDX ? 144 : 2048 + 512 + 2 * 33 * 4 + 8;
   static constexpr uint32_t kOutOff = kWarps * kRingBytes;
   static constexpr uint32_t kTabOff = kOutOff + kWarps * 2 * kStageOut;
   static constexpr uint32_t kBarOff = kTabOff + kWarps * kTabBytes;
