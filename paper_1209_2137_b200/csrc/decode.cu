@@ -86,7 +86,9 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
       const int64_t orow = tma_out && (ch.out_off & 31) == 0 ? (int64_t)(ch.out_off >> 5) : -1;
       const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
       uint4 carry = make_uint4(0, 0, 0, 0);
-      constexpr int ST = CODEC == IZG_SIMDFASTPFOR ? kVertical : kScalar;
+      constexpr int ST = CODEC == IZG_SIMDFASTPFOR ? kVertical
+                         : CODEC == IZG_FASTPFOR ? kScalar
+                                                 : kSimple8b;
       if (CODEC == IZG_SIMDBP128) {
         r.begin(p, ch.n_words);
         if (r.phase == 0)
@@ -197,7 +199,7 @@ KernelFn pick(int delta) {
 
 constexpr uint32_t kCounterSlots = 1024;
 static_assert(sizeof(FpScratch) <= Layout<IZG_SIMDFASTPFOR>::kTabBytes, "FpScratch layout");
-constexpr int kCodecs = 4;  // decoders: SIMD-BP128, SIMD-FastPFOR, BP32, FastPFOR
+constexpr int kCodecs = 5;  // SIMD-BP128, SIMD-FastPFOR, BP32, FastPFOR, SimplePFOR
 static_assert(Layout<IZG_SIMDFASTPFOR>::kTabBytes % 16 == 0, "FpScratch alignment");
 
 struct DeviceInfo {
@@ -278,7 +280,7 @@ namespace izg {
 int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* d_chunks,
                 uint32_t n_chunks, uint32_t* d_out, int32_t* d_status, uint32_t* d_consumed,
                 void* d_ws, uint64_t ws_bytes, void* stream) {
-  if (codec < IZG_SIMDBP128 || codec > IZG_FASTPFOR) return IZG_ERR_INVALID_ARGUMENT;
+  if (codec < IZG_SIMDBP128 || codec > IZG_SIMPLEPFOR) return IZG_ERR_INVALID_ARGUMENT;
   if (delta < IZG_DELTA_NONE || delta > IZG_DELTA_DM) return IZG_ERR_INVALID_ARGUMENT;
   if (n_chunks == 0) return IZG_SUCCESS;
   if (!d_words || !d_chunks || !d_out || !d_status) return IZG_ERR_INVALID_ARGUMENT;
@@ -290,7 +292,8 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   }
   const int dev = device_of(d_status);
   if (dev < 0) return IZG_ERR_INVALID_ARGUMENT;
-  const bool paged = codec == IZG_SIMDFASTPFOR || codec == IZG_FASTPFOR;
+  const bool paged = codec == IZG_SIMDFASTPFOR || codec == IZG_FASTPFOR ||
+                     codec == IZG_SIMPLEPFOR;
   // The indexed path serves SIMD-FastPFOR.  Scalar-array FastPFOR pages
   // decode with the fused kernel: its indexed variant faulted on pages with
   // exceptions in a code-layout-dependent way, so it is not
@@ -306,6 +309,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
       fn = idx ? pick<IZG_SIMDFASTPFOR, true>(delta) : pick<IZG_SIMDFASTPFOR, false>(delta);
       break;
     case IZG_FASTPFOR: fn = pick<IZG_FASTPFOR, false>(delta); break;
+    case IZG_SIMPLEPFOR: fn = pick<IZG_SIMPLEPFOR, false>(delta); break;
   }
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;

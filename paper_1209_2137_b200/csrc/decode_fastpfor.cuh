@@ -161,7 +161,135 @@ __device__ bool fp_positions_bad(const FpScratch& sc, const uint8_t* ba, uint32_
 }
 
 // Patch storage of the exception highs (codec_patched.cpp:195-199).
-enum { kVertical = 0, kScalar = 1 };
+enum { kVertical = 0, kScalar = 1, kSimple8b = 2 };
+
+// ---- Simple-8b exception highs (SimplePFOR) ------------------------------
+// One stream of 64-bit words (low half first) after the byte array
+// (codec_patched.cpp:284-287, 342-345); selector = low 4 bits, then
+// cap(sel) values of bits(sel) bits each (codec_basic.h:45-60); zero-run
+// selectors 0/1 code 240/120 zeros; values truncate to 32 bits
+// (simple8b_decode's 32-bit overload, codec_basic.cpp:227-300).
+__device__ __forceinline__ uint32_t s8_cap(uint32_t sel) {
+  const uint64_t lo = 0x0A0C0F141E3C78F0ull;  // sel 0..7: 240,120,60,30,20,15,12,10
+  const uint64_t hi = 0x0102030405060708ull;  // sel 8..15: 8,7,6,5,4,3,2,1
+  return (uint32_t)((sel < 8 ? lo : hi) >> (8 * (sel & 7))) & 0xFFu;
+}
+__device__ __forceinline__ uint32_t s8_bits(uint32_t sel) {
+  const uint64_t lo = 0x0605040302010000ull;  // sel 0..7: 0,0,1,2,3,4,5,6
+  const uint64_t hi = 0x3C1E140F0C0A0807ull;  // sel 8..15: 7,8,10,12,15,20,30,60
+  return (uint32_t)((sel < 8 ? lo : hi) >> (8 * (sel & 7))) & 0xFFu;
+}
+
+// simple8b_decode's bounds walk (codec_basic.cpp:296-305) over `T` values
+// from page word `pos`, 32 words per step: *end = first word after the last
+// word needed, or IZG_E_S8_EXHAUSTED when the page ends first.
+__device__ int32_t s8_scan(const uint32_t* page, uint32_t nw, uint32_t pos, uint32_t T, int lane,
+                           uint32_t* end) {
+  if (T == 0) {
+    *end = pos;
+    return IZG_OK;
+  }
+  uint32_t done = 0;
+  for (uint64_t k = 0;; k += 32) {
+    const uint64_t at = pos + 2 * (k + lane);
+    const bool valid = at + 2 <= nw;
+    const uint32_t cnt = valid ? s8_cap(ldg_u32(page + at) & 15u) : 0u;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const uint32_t hit = __ballot_sync(0xFFFFFFFFu, valid && done + incl >= T);
+    const uint32_t inv = __ballot_sync(0xFFFFFFFFu, !valid);
+    if (hit && (!inv || __ffs(hit) < __ffs(inv))) {
+      *end = (uint32_t)(pos + 2 * (k + __ffs(hit)));
+      return IZG_OK;
+    }
+    if (inv) return IZG_E_S8_EXHAUSTED;
+    done += __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+}
+
+// Window of 32 Simple-8b words (lane l holds word wk+l: halves and the value
+// index of its first value) over the stream at page word `pos`.
+struct S8Window {
+  uint32_t pos, nw;
+  uint32_t wk;     // stream word index of lane 0's word
+  uint32_t lo, hi, start, cnt, total;
+  __device__ __forceinline__ void load(const uint32_t* page, uint32_t k, uint32_t v0, int lane) {
+    wk = k;
+    const uint64_t at = pos + 2 * ((uint64_t)k + lane);
+    const bool valid = at + 2 <= nw;
+    lo = valid ? ldg_u32(page + at) : 0u;
+    hi = valid ? ldg_u32(page + at + 1) : 0u;
+    cnt = valid ? s8_cap(lo & 15u) : 0u;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    start = v0 + incl - cnt;
+    total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+  // Re-centre so that lane 0's word holds value e (e >= start of lane 0).
+  __device__ __forceinline__ void seek(const uint32_t* page, uint32_t e, int lane) {
+    uint32_t v0 = __shfl_sync(0xFFFFFFFFu, start, 0);
+    while (e >= v0 + total) {
+      load(page, wk + 32, v0 + total, lane);
+      v0 = __shfl_sync(0xFFFFFFFFu, start, 0);
+    }
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, start <= e && cnt);
+    const uint32_t l0 = m ? 31 - __clz(m) : 0u;
+    if (l0) load(page, wk + l0, __shfl_sync(0xFFFFFFFFu, start, l0), lane);
+  }
+};
+
+// Patch one warp iteration of a SimplePFOR page: its `tot` exceptions are
+// values E0 .. E0+tot-1 of the stream, dealt one per lane per round in block
+// order (blocks' exception prefixes p1 < p2 < p3 within the iteration).
+__device__ bool fp_patch_s8(uint32_t t, const uint32_t* page, const uint8_t* ba, S8Window& win,
+                            uint32_t E0, uint32_t tot, uint32_t myb, uint32_t myc, uint32_t mybp,
+                            int lane) {
+  const uint32_t p1 = __shfl_sync(0xFFFFFFFFu, myc, 0);
+  const uint32_t p2 = p1 + __shfl_sync(0xFFFFFFFFu, myc, 8);
+  const uint32_t p3 = p2 + __shfl_sync(0xFFFFFFFFu, myc, 16);
+  bool bad = false;
+#pragma unroll 1
+  for (uint32_t base = 0; base < tot; base += 32) {
+    win.seek(page, E0 + base, lane);
+    const uint32_t x = base + lane;  // exception index within the iteration
+    const bool ok = x < tot;
+    const uint32_t e = E0 + x;
+    uint32_t l = 0;  // last window word whose first value is <= e
+#pragma unroll
+    for (uint32_t st = 16; st; st >>= 1) {
+      const uint32_t v = __shfl_sync(0xFFFFFFFFu, win.start, (l + st) & 31);
+      if (l + st < 32 && v <= e) l += st;
+    }
+    const uint32_t wlo = __shfl_sync(0xFFFFFFFFu, win.lo, l);
+    const uint32_t whi = __shfl_sync(0xFFFFFFFFu, win.hi, l);
+    const uint32_t j = e - __shfl_sync(0xFFFFFFFFu, win.start, l);
+    const uint32_t q = (x >= p1) + (x >= p2) + (x >= p3);
+    const uint32_t b = __shfl_sync(0xFFFFFFFFu, myb, 8 * q);
+    const uint32_t bp = __shfl_sync(0xFFFFFFFFu, mybp, 8 * q);
+    if (ok) {
+      const uint32_t i = x - (q == 0 ? 0u : q == 1 ? p1 : q == 2 ? p2 : p3);
+      const uint32_t bits = s8_bits(wlo & 15u);
+      const uint64_t word = (uint64_t)whi << 32 | wlo;
+      const uint32_t high =
+          bits ? (uint32_t)((word >> (4 + j * bits)) & ((1ull << bits) - 1)) : 0u;
+      const uint32_t pp = ld_u8(ba + bp + i);
+      if (pp >= 128u)
+        bad = true;
+      else if (high)
+        asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(OutStage::swz(t, 128u * q + pp)),
+                     "r"(high << b));
+    }
+  }
+  return bad;
+}
 
 // Phase 2.  `pos` = page word after the byte array; *end = words consumed.
 // ST = kVertical: 16-byte-aligned vertical groups of 128 (simdfastpfor);
@@ -260,16 +388,26 @@ __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const
 
 // Phase 3.  Returns an izg_status; *bad_pos is set when a position >= 128
 // was met (the caller resolves precedence).
+// SimplePFOR (ST == kSimple8b): exceptions are consumed in block order from
+// one stream starting at page word `s8pos` (nw = page words), so a block's
+// cursor is the running exception count and there is no exhaustion check.
 template <int DELTA, int ST>
 __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uint32_t* page,
                              uint32_t A, uint32_t nblocks, uint32_t* out, bool oal, int64_t orow,
-                             uint4& carry, bool* bad_pos) {
+                             uint4& carry, bool* bad_pos, uint32_t s8pos = 0, uint32_t nw = 0) {
   const int lane = threadIdx.x & 31;
   const uint32_t q = lane >> 3, s8 = lane & 7;
   const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
   uint32_t packed = 1;  // page word of the next block's payload
   uint32_t bpos = 0;    // byte-array offset of the next block's entry
   uint32_t used = 0;    // lane w-1: exceptions consumed from array w
+  uint32_t E = 0;       // SimplePFOR: exceptions consumed so far
+  S8Window win;
+  if (ST == kSimple8b) {
+    win.pos = s8pos;
+    win.nw = nw;
+    win.load(page, 0, 0, lane);
+  }
   bool bad = false;
 #pragma unroll 1
   for (uint32_t g0 = 0; g0 < nblocks; g0 += 4) {
@@ -312,7 +450,7 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
     const uint32_t pk_ex = pk - 4u * b;
     // codec_patched.cpp:387-388 then 406-407, block by block
     const bool ov = (uint32_t)lane < ng && packed + pk > A;
-    const bool ex = c && cur + c > sc.dir_n[w];
+    const bool ex = ST != kSimple8b && c && cur + c > sc.dir_n[w];
     const uint32_t em = __ballot_sync(0xFFFFFFFFu, ov || ex) & 0xFu;
     if (em) {
       const int k = __ffs(em) - 1;
@@ -325,11 +463,13 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
     const uint32_t myw = __shfl_sync(0xFFFFFFFFu, w, q);
     const uint32_t mybp = __shfl_sync(0xFFFFFFFFu, bp, q);
     const uint32_t mycur = __shfl_sync(0xFFFFFFFFu, cur, q);
-    const uint32_t mybase = sc.dir_base[myw];
+    const uint32_t mybase = ST == kSimple8b ? 0u : sc.dir_base[myw];
     const uint32_t first = packed;
     packed += __shfl_sync(0xFFFFFFFFu, pk, 3);
     bpos += __shfl_sync(0xFFFFFFFFu, bl, 3);
     const uint32_t tot = __shfl_sync(0xFFFFFFFFu, ce, 3);
+    const uint32_t E0 = E;  // SimplePFOR: first stream value of this iteration
+    E += tot;
 
     // Stream window: packed words [first, packed) (the stream starts at word 1).
     r.release_below(4u * (first - 1));
@@ -347,7 +487,10 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
       const uint32_t t = os.acquire();
       OutStage::write(t, v, lane);
       __syncwarp();
-      bad |= fp_patch<ST>(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
+      if (ST == kSimple8b)
+        bad |= fp_patch_s8(t, page, ba, win, E0, tot, myb, myc, mybp, lane);
+      else
+        bad |= fp_patch<ST>(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
       __syncwarp();
       OutStage::read(t, v, lane);
       scan<DELTA>(v, carry, lane);
@@ -399,7 +542,16 @@ __device__ int32_t fastpfor_core(WarpRing& r, OutStage& os, FpScratch& sc, const
   if (st) return fp_positions_bad(sc, ba, parsed, lane) ? IZG_E_FP_POS_RANGE : st;
 
   uint32_t end = 0;
-  st = fp_directory<ST>(sc, page, nw, A + 1 + ba_words, lane, &end);
+  if (ST == kSimple8b) {
+    // simple8b_decode of all the page's highs up front (codec_patched.cpp:342-345)
+    uint32_t T = 0;
+    for (uint32_t k = lane; k < nblocks; k += 32) T += sc.tab[k] >> 12;
+#pragma unroll
+    for (int d = 16; d; d >>= 1) T += __shfl_xor_sync(0xFFFFFFFFu, T, d);
+    st = s8_scan(page, nw, A + 1 + (uint32_t)ba_words, T, lane, &end);
+  } else {
+    st = fp_directory<ST>(sc, page, nw, A + 1 + ba_words, lane, &end);
+  }
   if (st) return fp_positions_bad(sc, ba, nblocks, lane) ? IZG_E_FP_POS_RANGE : st;
 
   // exception arrays: warm L2 while the packed area streams
@@ -409,7 +561,8 @@ __device__ int32_t fastpfor_core(WarpRing& r, OutStage& os, FpScratch& sc, const
   }
   r.begin(page + 1, A - 1);
   bool bad_pos = false;
-  st = fp_blocks<DELTA, ST>(r, os, sc, page, A, nblocks, out, oal, orow, carry, &bad_pos);
+  st = fp_blocks<DELTA, ST>(r, os, sc, page, A, nblocks, out, oal, orow, carry, &bad_pos,
+                            A + 1 + (uint32_t)ba_words, nw);
   r.end();
   if (st) return fp_positions_bad(sc, ba, nblocks, lane) ? IZG_E_FP_POS_RANGE : st;
   if (bad_pos) return IZG_E_FP_POS_RANGE;

@@ -81,6 +81,8 @@ extern "C" int izg_parse_codec_name(const char* name, int* codec, int* delta) {
     *codec = IZG_BP32;
   else if (s == "fastpfor")
     *codec = IZG_FASTPFOR;
+  else if (s == "simplepfor")
+    *codec = IZG_SIMPLEPFOR;
   else
     return IZG_ERR_UNKNOWN_CODEC;
   *delta = d;

@@ -50,6 +50,7 @@ def test_codec_registry():
     assert P.make_codec("simdfastpfor-dm").delta == N.DELTA_DM
     # the scalar-group codecs of SURVEY.md §8 f3 (decode only)
     assert P.make_codec("bp32").codec == 2 and P.make_codec("fastpfor-s4").codec == 3
+    assert P.make_codec("simplepfor").codec == 4
     for bad in ("lz77", "", "simdbp128-s5", "vbyte", "pfor"):
         with pytest.raises(ValueError):
             P.make_codec(bad)

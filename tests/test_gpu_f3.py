@@ -1,9 +1,11 @@
 """GPU parity for the scalar-group codecs of SURVEY.md §8 f3 — BP32
-(codec_binpack.cpp:17-60) and FastPFOR with scalar exception arrays
-(codec_patched.cpp:292-417, PatchStorage::scalar_arrays) — against the
-reference (compiled from source) and the oracle.  Inputs are encoded by the
+(codec_binpack.cpp:17-60), FastPFOR with scalar exception arrays and
+SimplePFOR with a Simple-8b stream of exception highs (codec_patched.cpp
+:292-417, PatchStorage::scalar_arrays / simple8b) — against the reference
+(compiled from source) and the oracle.  Inputs are encoded by the
 reference itself; the bar is bit-exact outputs and identical per-chunk
-statuses, on the fused path and (FastPFOR) the indexed path.
+statuses, through the host entry point and the device entry point (both
+run the fused page kernel for these codecs).
 """
 import zlib
 
@@ -15,7 +17,7 @@ from tests.helpers import assorted_arrays, random_sorted
 
 pytestmark = pytest.mark.gpu
 
-NAMES = ["bp32", "bp32-s4", "fastpfor", "fastpfor-s4"]
+NAMES = ["bp32", "bp32-s4", "fastpfor", "fastpfor-s4", "simplepfor", "simplepfor-s4"]
 
 
 def outlier_sorted(rng, n, rate=0.08):
@@ -56,7 +58,7 @@ def test_reference_encoded_arrays(cuda, ref, name):
     assert np.array_equal(d, flat)
 
 
-@pytest.mark.parametrize("name", ["bp32", "fastpfor"])
+@pytest.mark.parametrize("name", ["bp32", "fastpfor", "simplepfor"])
 def test_decode_deltas_every_width(cuda, ref, name):
     """decode_deltas (raw) at every width 0..32, words consumed included."""
     codec = P.make_codec(name)
@@ -65,7 +67,7 @@ def test_decode_deltas_every_width(cuda, ref, name):
     for b in range(33):
         n = 128 * int(rng.integers(1, 20))
         v = (rng.integers(0, 2**32, size=n, dtype=np.uint64) & ((1 << b) - 1)).astype(np.uint32)
-        if b and name == "fastpfor":  # a few wide values: exceptions at every width
+        if b and name != "bp32":  # a few wide values: exceptions at every width
             v[rng.integers(0, n, size=3)] |= np.uint32(1 << (b - 1))
         payloads.append(ref.encode_deltas(name, v))
         counts.append(n)
@@ -106,18 +108,20 @@ def test_mutation_fuzz_matches_oracle(cuda, ref, oracle, name):
             assert np.array_equal(d[o:o + n], oout), i
 
 
-def test_fastpfor_scalar_structural_mutations(cuda, oracle):
-    """Every page field of a scalar-array FastPFOR page (the SIMD-FastPFOR
-    structural corpus of test_gpu_indexed, reused), both decode paths."""
+@pytest.mark.parametrize("name", ["fastpfor-s4", "simplepfor-s4"])
+def test_page_structural_mutations(cuda, oracle, name):
+    """Every page field of a scalar-group page (the SIMD-FastPFOR structural
+    corpus of test_gpu_indexed, reused: for SimplePFOR the "bitset" and
+    "count" words are the first Simple-8b word), both decode paths."""
     from tests.test_gpu_indexed import mutations
 
-    codec = P.make_codec("fastpfor-s4")
+    codec = P.make_codec(name)
     rng = np.random.default_rng(17)
     payloads, counts = [], []
     for n in (128, 700, 9000, 65536):
         from oracle.pyoracle import Reference
 
-        p = Reference().encode_array("fastpfor-s4", outlier_sorted(rng, n))[0][1]
+        p = Reference().encode_array(name, outlier_sorted(rng, n))[0][1]
         payloads.append(p)
         counts.append(n)
         for q in mutations(rng, p):
@@ -127,7 +131,7 @@ def test_fastpfor_scalar_structural_mutations(cuda, oracle):
     (h, hs), (d, ds, _) = decode_both(codec, enc)
     assert np.array_equal(hs, ds)
     for i, (p, n) in enumerate(zip(payloads, counts)):
-        ost, oout = oracle.decode_chunk("fastpfor-s4", p, n)
+        ost, oout = oracle.decode_chunk(name, p, n)
         assert hs[i] == ost, (i, hs[i], ost)
         if ost == 0:
             o = int(enc.table["out_off"][i])
