@@ -463,7 +463,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                    "path": "izg_decode_host (pinned host buffers, 3-stream pipelined copies)",
+                    "path": "izg_decode_host (pinned host buffers; H2D + decode on 4 slot streams, D2H split over 3 streams)",
                     "verified": e2e_ok},
             "clocks": clk,
             "gpu_launches": args.steps * sum(b.launches_per_decode for b in batches.values()),

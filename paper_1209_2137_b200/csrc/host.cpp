@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string_view>
 #include <vector>
@@ -123,11 +124,18 @@ struct Slot {
   int32_t* status = nullptr;
   uint8_t* ws = nullptr;  // izg_decode_ws workspace (SIMD-FastPFOR index pass)
   uint64_t ws_cap = 0;
+  cudaEvent_t decoded = nullptr;   // piece decoded: its D2H may start
+  cudaEvent_t drained[3] = {};     // piece's D2H parts done: the slot may be reused
 };
 
 struct Scratch {
   int device = -1;
   Slot slot[kSlots];
+  // device->host copies: each piece's output goes out as kParts concurrent
+  // copies on kParts streams (several copies in flight keep D2H, the
+  // pipeline's bottleneck, at ~56 GB/s instead of ~50 for one stream)
+  static constexpr int kParts = 3;
+  cudaStream_t d2h[kParts] = {};
   // pinned staging for the chunk table and the statuses, so every copy of
   // the pipeline is truly asynchronous (pageable copies block the host)
   izg_chunk* pin_table = nullptr;
@@ -145,9 +153,15 @@ struct Scratch {
       if (s.out) cudaFree(s.out);
       if (s.status) cudaFree(s.status);
       if (s.ws) cudaFree(s.ws);
+      if (s.decoded) cudaEventDestroy(s.decoded);
+      for (auto& e : s.drained)
+        if (e) cudaEventDestroy(e);
       if (s.stream) cudaStreamDestroy(s.stream);
       s = Slot{};
     }
+    for (auto& d : d2h)
+      if (d) cudaStreamDestroy(d);
+    for (auto& d : d2h) d = nullptr;
     device = -1;
   }
   ~Scratch() { release(); }
@@ -171,9 +185,10 @@ bool grow(T*& p, uint64_t& cap, uint64_t need) {
 
 extern "C" void izg_release_host_scratch(void) { t_scratch.release(); }
 
-// Pipelined over pieces of the chunk table on four streams, so the
-// host->device copy of piece k+1, the decode of piece k and the device->host
-// copy of piece k-1 overlap (separate copy engines).  Chunks must be ordered
+// Pipelined over pieces of the chunk table: H2D and decode of each piece on
+// one of four slot streams, every D2H on one stream in piece order (event
+// ordered), so the host->device copy of piece k+1, the decode of piece k and
+// the device->host copy of piece k-1 overlap on separate copy engines.  Chunks must be ordered
 // by word_off and out_off (as encode_array / izg_layout_chunks produce);
 // otherwise the whole batch is one piece.
 extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, uint64_t n_words,
@@ -193,8 +208,14 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     S.release();
     S.device = dev;
     for (auto& s : S.slot)
-      if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess)
+      if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s.decoded, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s.drained[0], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s.drained[1], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s.drained[2], cudaEventDisableTiming) != cudaSuccess)
         return IZG_ERR_CUDA;
+    for (auto& d : S.d2h)
+      if (cudaStreamCreateWithFlags(&d, cudaStreamNonBlocking) != cudaSuccess) return IZG_ERR_CUDA;
   }
   // Validate the table against the host buffers (bounds of the copies).
   bool ordered = true;
@@ -208,11 +229,16 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
   // Pieces of about 64 MiB of output (enough chunks per launch to fill the
   // GPU, small enough to keep both copy engines busy).
   std::vector<uint32_t> cuts{0};
+  static const uint64_t piece_ints = [] {
+    const char* e = std::getenv("IZG_HOST_PIECE_MI");  // tuning knob (integers, in Mi)
+    const long v = e ? std::atol(e) : 0;
+    return (uint64_t)(v > 0 ? v : 16) << 20;
+  }();
   if (ordered) {
     uint64_t acc = 0;
     for (uint32_t i = 0; i < n_chunks; ++i) {
       acc += h_chunks[i].n;
-      if (acc >= (uint64_t{16} << 20) && i + 1 < n_chunks) {
+      if (acc >= piece_ints && i + 1 < n_chunks) {
         cuts.push_back(i + 1);
         acc = 0;
       }
@@ -267,6 +293,7 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
       rc = IZG_ERR_INVALID_ARGUMENT;
       break;
     }
+    for (auto& e : s.drained) cudaStreamWaitEvent(s.stream, e, 0);  // previous D2H done
     cudaMemsetAsync(s.words + wcopy, 0, (wneed - wcopy) * 4, s.stream);
     cudaMemcpyAsync(s.words, h_words + wlo, wcopy * 4, cudaMemcpyHostToDevice, s.stream);
     cudaMemcpyAsync(s.table, S.pin_table + c0, sizeof(izg_chunk) * nc, cudaMemcpyHostToDevice,
@@ -278,12 +305,25 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
       rc = r;
       break;
     }
-    cudaMemcpyAsync(h_out + olo, s.out, (ohi - olo) * 4, cudaMemcpyDeviceToHost, s.stream);
-    cudaMemcpyAsync(st_host + c0, s.status, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost,
-                    s.stream);
+    cudaEventRecord(s.decoded, s.stream);
+    const uint64_t nout = ohi - olo, part = (nout / Scratch::kParts + 1023) & ~uint64_t{1023};
+    for (int k = 0; k < Scratch::kParts; ++k) {
+      cudaStreamWaitEvent(S.d2h[k], s.decoded, 0);
+      const uint64_t a = std::min<uint64_t>(nout, k * part);
+      const uint64_t b = k + 1 == Scratch::kParts ? nout : std::min<uint64_t>(nout, a + part);
+      if (b > a)
+        cudaMemcpyAsync(h_out + olo + a, s.out + a, (b - a) * 4, cudaMemcpyDeviceToHost,
+                        S.d2h[k]);
+      if (k == 0)
+        cudaMemcpyAsync(st_host + c0, s.status, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost,
+                        S.d2h[0]);
+      cudaEventRecord(s.drained[k], S.d2h[k]);
+    }
   }
   for (auto& s : S.slot)
     if (cudaStreamSynchronize(s.stream) != cudaSuccess) rc = IZG_ERR_CUDA;
+  for (auto& d : S.d2h)
+    if (cudaStreamSynchronize(d) != cudaSuccess) rc = IZG_ERR_CUDA;
   if (rc != IZG_SUCCESS) return rc;
   if (h_status) std::memcpy(h_status, st_host, sizeof(int32_t) * n_chunks);
   for (uint32_t i = 0; i < n_chunks; ++i)

@@ -26,3 +26,10 @@ for i in range(0, n, piece):
         h[i:i + piece].copy_(d[i:i + piece], non_blocking=True)
 torch.cuda.synchronize(); t = time.perf_counter() - t
 print("d2h 32MiB pieces", round(4 * n / t / 1e9, 1), "GB/s")
+# the e2e pattern: D2H of 4 B/int concurrent with H2D of ~1 B/int (C5 words)
+m = n // 4
+torch.cuda.synchronize(); t = time.perf_counter()
+with torch.cuda.stream(s1): h.copy_(d, non_blocking=True)
+with torch.cuda.stream(s2): d2[:m].copy_(h2[:m], non_blocking=True)
+torch.cuda.synchronize(); t = time.perf_counter() - t
+print("d2h 4GiB + concurrent h2d 1GiB:", round(4 * n / t / 1e9, 1), "GB/s d2h-equivalent")
