@@ -18,7 +18,10 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libintzip_b200.so")
 
-SOURCES = ["decode.cu", "host.cpp", "host_encode.cpp", "host_datagen.cpp", "container.cpp"]
+SOURCES = ["decode.cu", "decode_scalar.cu", "host.cpp", "host_encode.cpp", "host_datagen.cpp",
+           "container.cpp"]
+# per-source extra flags: see the comment at the top of decode_scalar.cu
+SOURCE_FLAGS = {"decode_scalar.cu": ["-Xptxas", "-O1"]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
@@ -49,7 +52,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
         extra = os.environ.get("IZG_NVCC_EXTRA", "").split()  # debug builds only
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *SOURCE_FLAGS.get(src, []), *extra, "-c",
+               os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")

@@ -72,7 +72,7 @@ struct __align__(16) FpScratch {
 // validated and tabulated lane-parallel, and the first failing entry (in
 // order) ends the walk with the reference's status.  *parsed = entries that
 // passed.
-__device__ int32_t fp_parse(WarpRing& r, FpScratch& sc, uint64_t L, uint32_t nblocks, int lane,
+static __device__ int32_t fp_parse(WarpRing& r, FpScratch& sc, uint64_t L, uint32_t nblocks, int lane,
                             uint32_t* parsed) {
   const uint32_t Lc = L > 0x7FFFFFF0ull ? 0x7FFFFFF0u : (uint32_t)L;
   uint32_t s = 0;   // next entry start (byte offset in the byte array)
@@ -148,7 +148,7 @@ __device__ int32_t fp_parse(WarpRing& r, FpScratch& sc, uint64_t L, uint32_t nbl
 // Slow path for error statuses: does any exception position of blocks
 // [0, nb) reach 128 (codec_patched.cpp:328-330)?  The reference validates
 // every position during its byte-array walk, before any later check.
-__device__ bool fp_positions_bad(const FpScratch& sc, const uint8_t* ba, uint32_t nb, int lane) {
+static __device__ bool fp_positions_bad(const FpScratch& sc, const uint8_t* ba, uint32_t nb, int lane) {
   bool bad = false;
   uint32_t bp = 0;  // entry start in the byte array
   for (uint32_t k = 0; k < nb; ++k) {
@@ -183,7 +183,7 @@ __device__ __forceinline__ uint32_t s8_bits(uint32_t sel) {
 // simple8b_decode's bounds walk (codec_basic.cpp:296-305) over `T` values
 // from page word `pos`, 32 words per step: *end = first word after the last
 // word needed, or IZG_E_S8_EXHAUSTED when the page ends first.
-__device__ int32_t s8_scan(const uint32_t* page, uint32_t nw, uint32_t pos, uint32_t T, int lane,
+static __device__ int32_t s8_scan(const uint32_t* page, uint32_t nw, uint32_t pos, uint32_t T, int lane,
                            uint32_t* end) {
   if (T == 0) {
     *end = pos;
@@ -249,7 +249,7 @@ struct S8Window {
 // Patch one warp iteration of a SimplePFOR page: its `tot` exceptions are
 // values E0 .. E0+tot-1 of the stream, dealt one per lane per round in block
 // order (blocks' exception prefixes p1 < p2 < p3 within the iteration).
-__device__ bool fp_patch_s8(uint32_t t, const uint32_t* page, const uint8_t* ba, S8Window& win,
+static __device__ bool fp_patch_s8(uint32_t t, const uint32_t* page, const uint8_t* ba, S8Window& win,
                             uint32_t E0, uint32_t tot, uint32_t myb, uint32_t myc, uint32_t mybp,
                             int lane) {
   const uint32_t p1 = __shfl_sync(0xFFFFFFFFu, myc, 0);
@@ -295,7 +295,7 @@ __device__ bool fp_patch_s8(uint32_t t, const uint32_t* page, const uint8_t* ba,
 // ST = kVertical: 16-byte-aligned vertical groups of 128 (simdfastpfor);
 // kScalar: scalar groups of 32, no alignment (fastpfor).
 template <int ST>
-__device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint32_t nw, uint64_t pos,
+static __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint32_t nw, uint64_t pos,
                                 int lane, uint32_t* end) {
   sc.dir_n[lane + 1] = 0;
   sc.dir_base[lane + 1] = 0;
@@ -487,6 +487,7 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
       const uint32_t t = os.acquire();
       OutStage::write(t, v, lane);
       __syncwarp();
+
       if (ST == kSimple8b)
         bad |= fp_patch_s8(t, page, ba, win, E0, tot, myb, myc, mybp, lane);
       else

@@ -60,7 +60,7 @@ __host__ __device__ inline IdxView idx_view(void* ws, uint32_t n_chunks) {
 // plus the warp's running per-width count `cnt`), and — when `checks` — the
 // block loop's overrun / exhaustion checks in block order
 // (codec_patched.cpp:387-388, 406-407).  Records go out coalesced.
-__device__ int32_t fp_meta(const FpScratch& sc, uint32_t* cnt, uint4* rec, uint32_t nb,
+static __device__ int32_t fp_meta(const FpScratch& sc, uint32_t* cnt, uint4* rec, uint32_t nb,
                            uint32_t A, bool checks, int lane, uint32_t* packed_end) {
   cnt[lane + 1] = 0;
   __syncwarp();
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kIdxWarps * 32)
 // Error paths: does any exception position of records [0, nb) reach 128
 // (codec_patched.cpp:328-330)?  Checked before every later error, as the
 // reference validates positions during its byte-array walk.
-__device__ bool fp_positions_bad_idx(const uint4* rec, const uint8_t* ba, uint32_t nb, int lane) {
+static __device__ bool fp_positions_bad_idx(const uint4* rec, const uint8_t* ba, uint32_t nb, int lane) {
   bool bad = false;
   for (uint32_t k = lane; k < nb; k += 32) {
     const uint4 e = rec[k];
