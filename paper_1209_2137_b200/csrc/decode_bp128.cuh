@@ -158,11 +158,31 @@ __device__ __forceinline__ void unpack_scalar_slots(const WarpRing& r, uint32_t 
   }
 }
 
+// One 32-integer scalar group "by value": lane l extracts value l (bits
+// [l*w, l*w+w) of the w-word stream at payload word `off`) and stores it at
+// integer 32*row + l of the warp's output tile `t`.  The tile row is uniform,
+// so the 128-byte swizzle (OutStage::swz) reduces to an XOR of the lane's
+// 16-byte chunk with row & 7; 32 consecutive integers of one row are
+// conflict-free.  `roff` = r.ring_off().
+__device__ __forceinline__ void scalar_group_to_tile(const WarpRing& r, uint32_t roff,
+                                                     uint32_t off, uint32_t w, uint32_t t,
+                                                     uint32_t row, int lane) {
+  const uint32_t bit = (uint32_t)lane * w;
+  const uint32_t a = roff + 4u * off + ((bit >> 5) << 2);  // unmasked ring byte of word 0
+  const uint32_t lo = lds32(r.base + (a & kRingMask));
+  const uint32_t hi = lds32(r.base + ((a + 4u) & kRingMask));
+  const uint32_t dst = t + (row << 7) + ((((uint32_t)lane >> 2) ^ (row & 7u)) << 4) +
+                       (((uint32_t)lane & 3u) << 2);
+  sts32(dst, funnel_r(lo, hi, bit & 31u) & low_mask(w));
+}
+
 // Bp32Codec::decode_deltas (codec_binpack.cpp:43-60) fused like bp128_core:
 // per 128 integers one descriptor word (byte g = width of scalar group g)
-// and the four groups.  The four descriptors of a warp iteration form a
-// short dependent chain (each position follows the previous meta-block's
-// payload); their checks run in the reference's order.
+// and the four groups.  Per warp iteration the four descriptors are read as
+// a short dependent chain with a one-instruction width check (__vcmpgtu4)
+// and a byte-sum bound check; only a failing descriptor re-runs the
+// reference's per-group checks in order.  The 16 groups are unpacked by
+// value into the output tile and read back in mapping C for the scan.
 template <int DELTA>
 __device__ int32_t bp32_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t nblocks,
                              uint32_t* out, bool out_aligned, int64_t orow, uint4& carry,
@@ -173,55 +193,65 @@ __device__ int32_t bp32_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t nb
 #pragma unroll 1
   for (uint32_t g0 = 0; g0 < nblocks; g0 += 4) {
     const uint32_t ng = min(4u, nblocks - g0);
-    const uint32_t first = pos;
     // everything before this iteration is consumed: free it first, so the
     // ring can take the whole iteration (<= 4 x 129 words) before ensure()
-    r.release_below(4u * first);
-    uint32_t mypay = 0, mywidth = 0;  // this lane's block q: payload word, width
-#pragma unroll 1
-    for (uint32_t k = 0; k < ng; ++k) {
-      if (pos >= nw) return IZG_E_BP32_TRUNC_DESC;
-      r.ensure(4u * (pos + 1));
-      const uint32_t d = lds32(r.word_addr(pos));
-      ++pos;
-      uint32_t at = pos, bad = IZG_OK;
+    r.release_below(4u * pos);
+    uint32_t desc[4], dpos[4];
 #pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const uint32_t w = (d >> (8 * g)) & 0xFFu;
-        if (bad == IZG_OK) {
-          if (w > 32) bad = IZG_E_BP32_WIDTH;
-          else if (at + w > nw) bad = IZG_E_BP32_TRUNC_PAYLOAD;
+    for (uint32_t k = 0; k < 4; ++k) {
+      desc[k] = 0;
+      dpos[k] = pos;
+      if (k < ng) {
+        if (pos >= nw) return IZG_E_BP32_TRUNC_DESC;
+        r.ensure(4u * (pos + 1));
+        const uint32_t d = lds32(r.word_addr(pos));
+        const uint32_t sum = __dp4a(d, 0x01010101u, 0u);  // the four widths
+        if (__vcmpgtu4(d, 0x20202020u) || pos + 1 + sum > nw) {
+          uint32_t at = pos + 1;  // codec_binpack.cpp:49-53, group by group
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            const uint32_t w = (d >> (8 * g)) & 0xFFu;
+            if (w > 32) return IZG_E_BP32_WIDTH;
+            if (at + w > nw) return IZG_E_BP32_TRUNC_PAYLOAD;
+            at += w;
+          }
         }
-        at += min(w, 33u);
+        desc[k] = d;
+        dpos[k] = pos + 1;
+        pos += 1 + sum;
       }
-      if (bad) return (int32_t)bad;
-      if (k == q) {
-        mypay = pos;
-        mywidth = d;
-      }
-      pos = at;
     }
     r.ensure(4u * pos);
-    // the lane's group s8/2 of block q: its width and payload word
-    const uint32_t gsel = s8 >> 1;
-    uint32_t width = 0, goff = 0;
+    const uint32_t t = os.acquire();
+    const uint32_t roff = r.ring_off();
 #pragma unroll
-    for (uint32_t g = 0; g < 4; ++g) {
-      const uint32_t w = (mywidth >> (8 * g)) & 0xFFu;
-      if (g == gsel) width = w;
-      if (g < gsel) goff += w;
+    for (uint32_t k = 0; k < 4; ++k) {
+      if (k < ng) {
+        uint32_t off = dpos[k];
+#pragma unroll
+        for (uint32_t g = 0; g < 4; ++g) {
+          const uint32_t w = (desc[k] >> (8 * g)) & 0xFFu;
+          scalar_group_to_tile(r, roff, off, w, t, 4u * k + g, lane);
+          off += w;
+        }
+      }
     }
-    const bool active = q < ng;
-    if (!active) width = 0;  // reads stay in the ring; values are zero
+    __syncwarp();
     uint32_t v[4][4];
-    // unpack_scalar_slots addresses group (s8 >> 1) as bword + gsel * width:
-    // pass the group's own start minus that offset
-    unpack_scalar_slots(r, mypay + goff - gsel * width, width, s8, v);
+    OutStage::read(t, v, lane);
+    const bool active = q < ng;
+    if (!active) {  // blocks past the end: zero deltas keep the carry exact
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[c][j] = 0;
+    }
     scan<DELTA>(v, carry, lane);
     if (orow >= 0 && ng == 4) {
-      os.put(v, lane, (uint32_t)(orow + 4 * g0));
-    } else if (active) {
-      store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, out_aligned);
+      os.commit(v, lane, (uint32_t)(orow + 4 * g0));
+    } else {
+      os.abandon();
+      if (active) store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, out_aligned);
     }
   }
   *pos_out = pos;
