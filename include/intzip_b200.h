@@ -211,6 +211,18 @@ int izg_encode(int codec, int delta, const uint32_t* d_values, izg_chunk* d_chun
 /* Words one chunk of n values can need (exact upper bound of the format). */
 uint64_t izg_encode_bound(int codec, uint32_t n);
 
+/* ---- consumer: intersection of decoded arrays ------- */
+/* Sorted intersection of two nondecreasing uint32 arrays in device memory
+ * (e.g. two posting lists decoded by izg_decode): the distinct values present
+ * in both, ascending (numpy.intersect1d semantics; the reference has no
+ * intersection API, PAPER.md:1697-1719 motivates it).  d_out holds
+ * min(n_a, n_b) words; *d_count (device) receives the number written.
+ * Stream-ordered; workspace of izg_intersect_workspace_size bytes. */
+uint64_t izg_intersect_workspace_size(uint64_t n_a, uint64_t n_b);
+int izg_intersect_sorted(const uint32_t* d_a, uint64_t n_a, const uint32_t* d_b,
+                         uint64_t n_b, uint32_t* d_out, uint64_t* d_count,
+                         void* d_workspace, uint64_t workspace_bytes, void* stream);
+
 /* ---- host entry points (synchronous, host buffers) -------------------- */
 
 /* decode_array over a batch of chunks held in HOST memory: copies the words

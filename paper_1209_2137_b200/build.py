@@ -18,8 +18,8 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libintzip_b200.so")
 
-SOURCES = ["decode.cu", "decode_scalar.cu", "host.cpp", "host_encode.cpp", "host_datagen.cpp",
-           "container.cpp"]
+SOURCES = ["decode.cu", "decode_scalar.cu", "intersect.cu", "host.cpp", "host_encode.cpp",
+           "host_datagen.cpp", "container.cpp"]
 # per-source extra flags: see the comment at the top of decode_scalar.cu
 SOURCE_FLAGS = {"decode_scalar.cu": ["-Xptxas", "-O1"]}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

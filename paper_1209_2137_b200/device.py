@@ -139,3 +139,36 @@ def encode_on_device(codec: Codec, values, value_off, counts, *, allow_wrap: boo
     out_table["out_off"] = value_off
     enc = Encoded(d_words.cpu().numpy().view(np.uint32), out_table)
     return enc, d_status[:len(counts)].cpu().numpy()
+
+
+def intersect_device(a, b, stream=None):
+    """Sorted intersection (numpy.intersect1d semantics) of two nondecreasing
+    int32/uint32 CUDA tensors on the device (izg_intersect_sorted); returns a
+    CUDA tensor of the common values.  The consumer of SURVEY.md §8 f4."""
+    import torch
+
+    dev = a.device
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    na, nb = a.numel(), b.numel()
+    out = torch.empty(max(min(na, nb), 1), dtype=torch.int32, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(N.lib().izg_intersect_workspace_size(na, nb), dtype=torch.uint8, device=dev)
+    rc = N.lib().izg_intersect_sorted(N.ptr(a) if na else None, na, N.ptr(b) if nb else None, nb,
+                                      N.ptr(out), N.ptr(count), N.ptr(ws), ws.numel(),
+                                      s.cuda_stream)
+    if rc != N.SUCCESS:
+        raise RuntimeError(f"izg_intersect_sorted failed: {rc}")
+    return out[:int(count.item())]
+
+
+def intersect(codec: Codec, enc_a: Encoded, enc_b: Encoded, device=None) -> np.ndarray:
+    """Decode two encoded arrays (posting lists) on the GPU and intersect them
+    there; only the intersection is copied back (numpy.intersect1d result)."""
+    ba = DeviceBatch(codec, enc_a, device)
+    bb = DeviceBatch(codec, enc_b, device)
+    ba.decode()
+    bb.decode()
+    ba.check()
+    bb.check()
+    r = intersect_device(ba.out[:ba.n_out], bb.out[:bb.n_out])
+    return r.cpu().numpy().view(np.uint32)
