@@ -223,6 +223,23 @@ int izg_intersect_sorted(const uint32_t* d_a, uint64_t n_a, const uint32_t* d_b,
                          uint64_t n_b, uint32_t* d_out, uint64_t* d_count,
                          void* d_workspace, uint64_t workspace_bytes, void* stream);
 
+/* Fused decode -> intersect: decodes the chunks (codec as izg_decode, delta
+ * IZG_DELTA_D1 or IZG_DELTA_D4, array mode) and intersects the decoded
+ * values with the nondecreasing device list d_s WITHOUT writing the decoded
+ * integers anywhere: each decoded tile is merged against d_s in shared
+ * memory.  d_out (n_s words) receives the distinct values present both in
+ * d_s and in the decoded chunks, ascending; *d_count (device) their number.
+ * Each chunk's decoded values must be nondecreasing (sorted lists, as D1/D4
+ * encode them); chunks may come from one array or several.  d_status gets
+ * the per-chunk statuses izg_decode would give; the result is meaningful
+ * only when all are IZG_OK.  chunk.out_off is ignored.  Stream-ordered;
+ * workspace of izg_decode_intersect_workspace_size(n_s) bytes. */
+uint64_t izg_decode_intersect_workspace_size(uint64_t n_s);
+int izg_decode_intersect(int codec, int delta, const uint32_t* d_words,
+                         const izg_chunk* d_chunks, uint32_t n_chunks, const uint32_t* d_s,
+                         uint64_t n_s, uint32_t* d_out, uint64_t* d_count, int32_t* d_status,
+                         void* d_workspace, uint64_t workspace_bytes, void* stream);
+
 /* ---- host entry points (synchronous, host buffers) -------------------- */
 
 /* decode_array over a batch of chunks held in HOST memory: copies the words

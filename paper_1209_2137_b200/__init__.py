@@ -9,10 +9,10 @@ from .codec import (CHUNK_SIZE, Codec, CorruptError, Encoded, codec_names, decod
                     raise_for_status)
 from .container import (Container, decode_container, read_container, read_raw_container,
                         scan_container)
-from .device import DeviceBatch, intersect, intersect_device
+from .device import DeviceBatch, decode_intersect_device, intersect, intersect_device
 
 __all__ = ["CHUNK_SIZE", "Codec", "Container", "CorruptError", "DeviceBatch", "Encoded",
-           "codec_names", "decode_container", "intersect", "intersect_device", "read_container", "read_raw_container",
+           "codec_names", "decode_container", "decode_intersect_device", "intersect", "intersect_device", "read_container", "read_raw_container",
            "scan_container",
            "decode_array", "encode_array", "encode_chunks", "gen_arrays", "layout",
            "make_codec", "raise_for_status", "_native"]

@@ -71,6 +71,11 @@ def lib() -> C.CDLL:
     L.izg_intersect_sorted.restype = C.c_int
     L.izg_intersect_sorted.argtypes = [vp, C.c_uint64, vp, C.c_uint64, vp, vp, vp, C.c_uint64,
                                        vp]
+    L.izg_decode_intersect_workspace_size.restype = C.c_uint64
+    L.izg_decode_intersect_workspace_size.argtypes = [C.c_uint64]
+    L.izg_decode_intersect.restype = C.c_int
+    L.izg_decode_intersect.argtypes = [C.c_int, C.c_int, vp, vp, C.c_uint32, vp, C.c_uint64, vp,
+                                       vp, vp, vp, C.c_uint64, vp]
     L.izg_checksum.restype = C.c_int
     L.izg_checksum.argtypes = [vp, C.c_uint64, vp, vp]
     L.izg_decode_host.restype = C.c_int
@@ -105,7 +110,8 @@ ABI_SYMBOLS = ("izg_status_string", "izg_parse_codec_name", "izg_layout_chunks",
                "izg_decode", "izg_decode_ws", "izg_decode_workspace_size", "izg_checksum", "izg_decode_host", "izg_release_host_scratch",
                "izg_encode", "izg_encode_bound", "izg_container_scan", "izg_container_index",
                "izg_container_decode_host", "izg_intersect_workspace_size",
-               "izg_intersect_sorted")
+               "izg_intersect_sorted", "izg_decode_intersect_workspace_size",
+               "izg_decode_intersect")
 
 
 def ptr(a) -> int:

@@ -8,6 +8,7 @@ cudart is linked statically so the .so is self-contained on the GPU box.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import os
 import subprocess
 import sys
@@ -18,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libintzip_b200.so")
 
-SOURCES = ["decode.cu", "decode_scalar.cu", "intersect.cu", "host.cpp", "host_encode.cpp",
+SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "intersect.cu", "host.cpp", "host_encode.cpp",
            "host_datagen.cpp", "container.cpp"]
 # per-source extra flags: see the comment at the top of decode_scalar.cu
 SOURCE_FLAGS = {"decode_scalar.cu": ["-Xptxas", "-O1"]}
@@ -48,13 +49,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(LIBDIR, "obj")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    extra = os.environ.get("IZG_NVCC_EXTRA", "").split()  # debug builds only
+
+    def compile_one(src):
         obj = os.path.join(objdir, src + ".o")
-        extra = os.environ.get("IZG_NVCC_EXTRA", "").split()  # debug builds only
         cmd = [NVCC, *ARCH, *FLAGS, *SOURCE_FLAGS.get(src, []), *extra, "-c",
                os.path.join(CSRC, src), "-o", obj]
-        res = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    jobs = max(1, min(len(SOURCES), os.cpu_count() or 1))
+    with concurrent.futures.ThreadPoolExecutor(jobs) as pool:
+        results = list(pool.map(compile_one, SOURCES))
+    objs = []
+    for src, obj, res in results:
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr}")
         if verbose:

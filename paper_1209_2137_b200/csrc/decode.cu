@@ -77,6 +77,8 @@ bool make_out_map(CUtensorMap* m, uint32_t* out) {
 // Scalar-array FastPFOR kernels live in decode_scalar.cu (ptxas -O1, see
 // there); every other decode kernel is instantiated in this file.
 KernelFn pick_fastpfor_scalar(int delta);
+// Probe-sink (decode -> intersect) kernels: decode_probe.cu.
+KernelFn pick_probe_kernel(int codec, int delta);
 
 
 constexpr uint32_t kCounterSlots = 1024;
@@ -88,7 +90,8 @@ struct DeviceInfo {
   bool init = false;
   bool ok = false;
   int sms = 0;
-  int occ[2 * kCodecs][5] = {};  // [codec (+ kCodecs: indexed page path)][delta]
+  // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink)][delta]
+  int occ[3 * kCodecs][5] = {};
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -107,7 +110,8 @@ int device_of(const void* p) {
   return a.device;
 }
 
-// `variant` = codec, + kCodecs for the indexed page decode kernels.
+// `variant` = codec, + kCodecs for the indexed page decode kernels, + 2 kCodecs
+// for the probe-sink kernels.
 int prepare(int dev, int variant, int delta, KernelFn fn, int threads, size_t smem,
             int* grid_per_sm, int* sms, uint32_t** counter) {
   if (dev < 0 || dev >= 64) return IZG_ERR_INVALID_ARGUMENT;
@@ -159,13 +163,16 @@ struct DeviceGuard {
 
 namespace izg {
 
+// `probe` non-null: decode -> intersect (ProbeStage sink, no output; d_out
+// is unused and the indexed path is not taken).
 int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* d_chunks,
                 uint32_t n_chunks, uint32_t* d_out, int32_t* d_status, uint32_t* d_consumed,
-                void* d_ws, uint64_t ws_bytes, void* stream) {
+                void* d_ws, uint64_t ws_bytes, void* stream, const ProbeArgs* probe = nullptr) {
   if (codec < IZG_SIMDBP128 || codec > IZG_SIMPLEPFOR) return IZG_ERR_INVALID_ARGUMENT;
   if (delta < IZG_DELTA_NONE || delta > IZG_DELTA_DM) return IZG_ERR_INVALID_ARGUMENT;
+  if (probe && delta != IZG_DELTA_D1 && delta != IZG_DELTA_D4) return IZG_ERR_INVALID_ARGUMENT;
   if (n_chunks == 0) return IZG_SUCCESS;
-  if (!d_words || !d_chunks || !d_out || !d_status) return IZG_ERR_INVALID_ARGUMENT;
+  if (!d_words || !d_chunks || (!d_out && !probe) || !d_status) return IZG_ERR_INVALID_ARGUMENT;
   if (reinterpret_cast<uintptr_t>(d_words) & 15) return IZG_ERR_INVALID_ARGUMENT;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -180,7 +187,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   // decode with the fused kernel: its indexed variant faulted on pages with
   // exceptions in a code-layout-dependent way, so it is not
   // built until that is understood.
-  const bool idx = codec == IZG_SIMDFASTPFOR && d_ws &&
+  const bool idx = !probe && codec == IZG_SIMDFASTPFOR && d_ws &&
                    (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
                    ws_bytes >= idx_workspace_bytes(n_chunks);
   KernelFn fn = nullptr;
@@ -193,6 +200,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     case IZG_FASTPFOR: fn = pick_fastpfor_scalar(delta); break;
     case IZG_SIMPLEPFOR: fn = pick<IZG_SIMPLEPFOR, false>(delta); break;
   }
+  if (probe) fn = pick_probe_kernel(codec, delta);
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;
   uint32_t* counter = nullptr;
@@ -200,7 +208,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   const size_t smem = idx     ? Layout<IZG_SIMDFASTPFOR, true>::kSmem
                       : paged ? Layout<IZG_SIMDFASTPFOR>::kSmem
                               : Layout<IZG_SIMDBP128>::kSmem;
-  int rc = prepare(dev, codec + (idx ? kCodecs : 0), delta, fn, warps * 32, smem, &per_sm, &sms,
+  int rc = prepare(dev, codec + (idx ? kCodecs : probe ? 2 * kCodecs : 0), delta, fn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -226,9 +234,9 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
   CUtensorMap omap;
   std::memset(&omap, 0, sizeof(omap));
-  const int tma_out = make_out_map(&omap, d_out) ? 1 : 0;
+  const int tma_out = !probe && make_out_map(&omap, d_out) ? 1 : 0;
   fn<<<grid, warps * 32, smem, s>>>(d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
-                                    counter, omap, tma_out, ix);
+                                    counter, omap, tma_out, ix, probe ? *probe : ProbeArgs{});
   return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
 }
 
@@ -239,6 +247,43 @@ extern "C" int izg_decode(int codec, int delta, const uint32_t* d_words,
                           int32_t* d_status, uint32_t* d_consumed, void* stream) {
   return izg::decode_impl(codec, delta, d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
                           nullptr, 0, stream);
+}
+
+namespace izg {
+// intersect.cu: hit bits of the probe list -> sorted distinct values
+int compact_hits(const uint32_t* d_s, uint64_t n_s, const uint32_t* hits, uint32_t* tiles,
+                 uint32_t* d_out, uint64_t* d_count, cudaStream_t s);
+uint64_t hit_words(uint64_t n_s);
+uint64_t compact_tiles(uint64_t n_s);
+}  // namespace izg
+
+extern "C" uint64_t izg_decode_intersect_workspace_size(uint64_t n_s) {
+  return 4 * (izg::hit_words(n_s) + izg::compact_tiles(n_s)) + 16;
+}
+
+extern "C" int izg_decode_intersect(int codec, int delta, const uint32_t* d_words,
+                                    const izg_chunk* d_chunks, uint32_t n_chunks,
+                                    const uint32_t* d_s, uint64_t n_s, uint32_t* d_out,
+                                    uint64_t* d_count, int32_t* d_status, void* d_ws,
+                                    uint64_t ws_bytes, void* stream) {
+  using namespace izg;
+  if (!d_count || (n_s && (!d_s || !d_out)) || !d_ws ||
+      ws_bytes < izg_decode_intersect_workspace_size(n_s) ||
+      (reinterpret_cast<uintptr_t>(d_ws) & 3))
+    return IZG_ERR_INVALID_ARGUMENT;
+  if (delta != IZG_DELTA_D1 && delta != IZG_DELTA_D4) return IZG_ERR_INVALID_ARGUMENT;
+  const int dev = device_of(d_count);
+  if (dev < 0) return IZG_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(dev);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint32_t* hits = static_cast<uint32_t*>(d_ws);
+  uint32_t* tiles = hits + hit_words(n_s);
+  if (cudaMemsetAsync(hits, 0, 4 * hit_words(n_s), s) != cudaSuccess) return IZG_ERR_CUDA;
+  const ProbeArgs pa{d_s, n_s, hits};
+  const int rc = decode_impl(codec, delta, d_words, d_chunks, n_chunks, nullptr, d_status,
+                             nullptr, nullptr, 0, stream, &pa);
+  if (rc != IZG_SUCCESS) return rc;
+  return compact_hits(d_s, n_s, hits, tiles, d_out, d_count, s);
 }
 
 extern "C" uint64_t izg_decode_workspace_size(int codec, uint32_t n_chunks) {

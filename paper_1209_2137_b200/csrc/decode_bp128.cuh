@@ -183,8 +183,8 @@ __device__ __forceinline__ void scalar_group_to_tile(const WarpRing& r, uint32_t
 // and a byte-sum bound check; only a failing descriptor re-runs the
 // reference's per-group checks in order.  The 16 groups are unpacked by
 // value into the output tile and read back in mapping C for the scan.
-template <int DELTA>
-__device__ int32_t bp32_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t nblocks,
+template <int DELTA, typename OS>
+__device__ int32_t bp32_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks,
                              uint32_t* out, bool out_aligned, int64_t orow, uint4& carry,
                              uint32_t* pos_out) {
   const int lane = threadIdx.x & 31;
@@ -251,7 +251,7 @@ __device__ int32_t bp32_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t nb
       os.commit(v, lane, (uint32_t)(orow + 4 * g0));
     } else {
       os.abandon();
-      if (active) store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, out_aligned);
+      os.direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, out_aligned, active, 128u * ng, lane);
     }
   }
   *pos_out = pos;
@@ -262,8 +262,8 @@ __device__ int32_t bp32_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t nb
 // Returns an izg_status; on success *pos_out = payload words consumed.
 // `orow` is the chunk's first output row (32 integers) for the TMA path, or
 // -1 when the output is not 128-byte aligned (direct stores then).
-template <int DELTA, bool ALIGNED>
-__device__ int32_t bp128_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t nblocks,
+template <int DELTA, bool ALIGNED, typename OS>
+__device__ int32_t bp128_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks,
                               uint32_t* out, bool out_aligned, int64_t orow, uint4& carry,
                               uint32_t* pos_out) {
   const int lane = threadIdx.x & 31;
@@ -298,8 +298,9 @@ __device__ int32_t bp128_core(WarpRing& r, OutStage& os, uint32_t nw, uint32_t n
       scan<DELTA>(v, carry, lane);
       if (orow >= 0 && g0 + 4 <= groups) {
         os.put(v, lane, (uint32_t)(orow + 4 * (mb0 + g0)));
-      } else if (active) {
-        store_direct(v, out + (size_t)(mb0 + gi) * 128 + 16 * s8, out_aligned);
+      } else {
+        os.direct(v, out + (size_t)(mb0 + gi) * 128 + 16 * s8, out_aligned, active,
+                  128u * min(4u, groups - g0), lane);
       }
     }
     pos = pay + m.size;

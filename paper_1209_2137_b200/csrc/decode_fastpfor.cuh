@@ -391,8 +391,8 @@ __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const
 // SimplePFOR (ST == kSimple8b): exceptions are consumed in block order from
 // one stream starting at page word `s8pos` (nw = page words), so a block's
 // cursor is the running exception count and there is no exhaustion check.
-template <int DELTA, int ST>
-__device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uint32_t* page,
+template <int DELTA, int ST, typename OS>
+__device__ int32_t fp_blocks(WarpRing& r, OS& os, FpScratch& sc, const uint32_t* page,
                              uint32_t A, uint32_t nblocks, uint32_t* out, bool oal, int64_t orow,
                              uint4& carry, bool* bad_pos, uint32_t s8pos = 0, uint32_t nw = 0) {
   const int lane = threadIdx.x & 31;
@@ -499,14 +499,14 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
         os.commit(v, lane, (uint32_t)(orow + 4 * g0));
       } else {
         os.abandon();
-        if (live) store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal);
+        os.direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal, live, 128u * ng, lane);
       }
     } else {
       scan<DELTA>(v, carry, lane);
       if (orow >= 0 && ng == 4)
         os.put(v, lane, (uint32_t)(orow + 4 * g0));
-      else if (live)
-        store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal);
+      else
+        os.direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal, live, 128u * ng, lane);
     }
   }
   *bad_pos = __any_sync(0xFFFFFFFFu, bad);
@@ -515,8 +515,8 @@ __device__ int32_t fp_blocks(WarpRing& r, OutStage& os, FpScratch& sc, const uin
 }
 
 // Whole page.  `nblocks` = count / 128; *pos_out = words consumed.
-template <int DELTA, int ST>
-__device__ int32_t fastpfor_core(WarpRing& r, OutStage& os, FpScratch& sc, const uint32_t* page,
+template <int DELTA, int ST, typename OS>
+__device__ int32_t fastpfor_core(WarpRing& r, OS& os, FpScratch& sc, const uint32_t* page,
                                  uint32_t nw, uint32_t nblocks, uint32_t* out, bool oal,
                                  int64_t orow, uint4& carry, uint32_t* pos_out) {
   const int lane = threadIdx.x & 31;

@@ -17,6 +17,7 @@
 #include "decode_fastpfor.cuh"
 #include "index_fastpfor.cuh"
 #include "izg_common.cuh"
+#include "probe.cuh"
 
 namespace izg {
 
@@ -37,14 +38,17 @@ __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t
 // Persistent kernel: every warp repeatedly claims the next chunk (one atomic
 // per chunk) and decodes it end to end: stream, unpack, patch, prefix sum,
 // VByte remainder, consumption check, status.  IDX (SIMD-FastPFOR only):
-// pages were indexed by fp_index_kernel into `ix`.
-template <int CODEC, int DELTA, bool IDX>
+// pages were indexed by fp_index_kernel into `ix`.  OS is the output sink:
+// OutStage writes the decoded integers to `out`; ProbeStage (probe.cuh)
+// intersects them with `pa.s` instead and `out` is unused.
+template <int CODEC, int DELTA, bool IDX, typename OS = OutStage>
 __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
     __maxnreg__((Layout<CODEC, IDX>::kMaxRegs))
     decode_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                   uint32_t n_chunks, uint32_t* __restrict__ out, int32_t* __restrict__ status,
                   uint32_t* __restrict__ consumed, uint32_t* __restrict__ next_chunk,
-                  const __grid_constant__ CUtensorMap omap, int tma_out, IdxView ix) {
+                  const __grid_constant__ CUtensorMap omap, int tma_out, IdxView ix,
+                  ProbeArgs pa) {
   extern __shared__ __align__(1024) uint8_t smem[];
   using LY = Layout<CODEC, IDX>;
   constexpr bool kArray = DELTA != IZG_DELTA_NONE;
@@ -54,11 +58,15 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
   r.base = smem_u32(r.gen);
   r.full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff) + warp * kNS;
   FpScratch* fsc = reinterpret_cast<FpScratch*>(smem + LY::kTabOff + warp * LY::kTabBytes);
-  OutStage os;
+  OS os;
   os.base = smem_u32(smem + LY::kOutOff + warp * 2 * kStageOut);
-  os.buf = 0;
-  os.tmap = &omap;
   os.leader = lane == 0;
+  if constexpr (OS::kProbe) {
+    os.pa = pa;
+  } else {
+    os.buf = 0;
+    os.tmap = &omap;
+  }
   r.g = 0;
   r.leader = lane == 0;
   r.policy = policy_evict_first();
@@ -76,11 +84,15 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
     const izg_chunk ch = chunks[c];
     int32_t st = precheck(CODEC, kArray, ch.n);
     uint32_t pos = 0;
+    os.begin_chunk();
     if (st == IZG_OK) {
       const uint32_t* p = words + ch.word_off;
-      uint32_t* o = out + ch.out_off;
+      // probe sink: no output; every full iteration takes the put/commit path
+      uint32_t* o = OS::kProbe ? nullptr : out + ch.out_off;
       const bool oal = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
-      const int64_t orow = tma_out && (ch.out_off & 31) == 0 ? (int64_t)(ch.out_off >> 5) : -1;
+      const int64_t orow = OS::kProbe                                ? 0
+                           : tma_out && (ch.out_off & 31) == 0 ? (int64_t)(ch.out_off >> 5)
+                                                                   : -1;
       const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
       uint4 carry = make_uint4(0, 0, 0, 0);
       constexpr int ST = CODEC == IZG_SIMDFASTPFOR ? kVertical
@@ -109,12 +121,35 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
         if (core < ch.n) {
           // Variable Byte remainder (codec.cpp:56-62).
           uint32_t rb = 0;
+          const uint32_t cnt = ch.n - core;
+          // probe sink: the tail goes to the warp's second (idle) tile,
+          // linear, then through the probe like any short iteration
+          // (vbyte_tail writes out[core + i], hence the offset base)
+          uint32_t* tail = nullptr;
+          if constexpr (OS::kProbe)
+            tail = reinterpret_cast<uint32_t*>(smem + LY::kOutOff + warp * 2 * kStageOut +
+                                               kStageOut);
           if (lane == 0)
             st = vbyte_tail<DELTA>(reinterpret_cast<const uint8_t*>(p + pos),
-                                   4u * (ch.n_words - pos), core, ch.n - core, carry, o, &rb);
+                                   4u * (ch.n_words - pos), core, cnt, carry,
+                                   OS::kProbe ? tail - core : o, &rb);
           st = __shfl_sync(0xFFFFFFFFu, st, 0);
           rb = __shfl_sync(0xFFFFFFFFu, rb, 0);
           if (st == IZG_OK) pos += (rb + 3) / 4;
+          if constexpr (OS::kProbe) {
+            if (st == IZG_OK) {
+              __syncwarp();
+              uint32_t v[4][4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const uint32_t i = 16u * lane + 4u * k + j;
+                  v[k][j] = i < cnt ? tail[i] : 0u;
+                }
+              os.direct(v, nullptr, false, true, cnt, lane);
+            }
+          }
         }
         if (st == IZG_OK && pos != ch.n_words) st = IZG_E_PAYLOAD_SIZE;  // codec.cpp:63-64
       }
@@ -128,7 +163,7 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
 }
 
 using KernelFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
-                          uint32_t*, uint32_t*, const CUtensorMap, int, IdxView);
+                          uint32_t*, uint32_t*, const CUtensorMap, int, IdxView, ProbeArgs);
 
 template <int CODEC, bool IDX>
 KernelFn pick(int delta) {
@@ -138,6 +173,20 @@ KernelFn pick(int delta) {
     case IZG_DELTA_D4: return decode_kernel<CODEC, IZG_DELTA_D4, IDX>;
     case IZG_DELTA_D2: return decode_kernel<CODEC, IZG_DELTA_D2, IDX>;
     case IZG_DELTA_DM: return decode_kernel<CODEC, IZG_DELTA_DM, IDX>;
+  }
+  return nullptr;
+}
+
+}  // namespace izg
+
+namespace izg {
+
+// Probe-sink kernels (decode -> intersect), array modes D1 / D4 only.
+template <int CODEC>
+KernelFn pick_probe(int delta) {
+  switch (delta) {
+    case IZG_DELTA_D1: return decode_kernel<CODEC, IZG_DELTA_D1, false, ProbeStage>;
+    case IZG_DELTA_D4: return decode_kernel<CODEC, IZG_DELTA_D4, false, ProbeStage>;
   }
   return nullptr;
 }

@@ -18,5 +18,6 @@
 namespace izg {
 
 KernelFn pick_fastpfor_scalar(int delta) { return pick<IZG_FASTPFOR, false>(delta); }
+KernelFn pick_probe_fastpfor_scalar(int delta) { return pick_probe<IZG_FASTPFOR>(delta); }
 
 }  // namespace izg

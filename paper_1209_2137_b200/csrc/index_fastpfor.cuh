@@ -199,8 +199,8 @@ static __device__ bool fp_positions_bad_idx(const uint4* rec, const uint8_t* ba,
 // index pass already made): as fp_blocks, but each lane reads its block's
 // record (lanes 8q..8q+7 share block q's 16 bytes) one iteration ahead.
 // Returns true when an exception position >= 128 was met.
-template <int DELTA, int ST>
-__device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const uint32_t* dir_base, const uint4* rec,
+template <int DELTA, int ST, typename OS>
+__device__ bool fp_blocks_idx(WarpRing& r, OS& os, const uint32_t* dir_base, const uint4* rec,
                               const uint32_t* page, uint32_t A, uint32_t nblocks, uint32_t* out,
                               bool oal, int64_t orow, uint4& carry) {
   const int lane = threadIdx.x & 31;
@@ -245,14 +245,14 @@ __device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const uint32_t* dir_bas
         os.commit(v, lane, (uint32_t)(orow + 4 * g0));
       } else {
         os.abandon();
-        if (live) store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal);
+        os.direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal, live, 128u * ng, lane);
       }
     } else {
       scan<DELTA>(v, carry, lane);
       if (orow >= 0 && ng == 4)
         os.put(v, lane, (uint32_t)(orow + 4 * g0));
-      else if (live)
-        store_direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal);
+      else
+        os.direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal, live, 128u * ng, lane);
     }
   }
   return __any_sync(0xFFFFFFFFu, bad);
@@ -260,8 +260,8 @@ __device__ bool fp_blocks_idx(WarpRing& r, OutStage& os, const uint32_t* dir_bas
 
 // Whole indexed page `c` (record written by fp_index_kernel); same contract
 // as fastpfor_core.
-template <int DELTA, int ST>
-__device__ int32_t fastpfor_core_idx(WarpRing& r, OutStage& os, uint32_t* dir_base,
+template <int DELTA, int ST, typename OS>
+__device__ int32_t fastpfor_core_idx(WarpRing& r, OS& os, uint32_t* dir_base,
                                      const uint32_t* page, uint32_t c, uint32_t nblocks,
                                      const IdxView& ix, uint32_t* out, bool oal, int64_t orow,
                                      uint4& carry, uint32_t* pos_out) {

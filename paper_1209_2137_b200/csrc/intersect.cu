@@ -113,7 +113,99 @@ __global__ void __launch_bounds__(kThreads)
     if (m >> k & 1u) out[o++] = __ldg(a + base + k);
 }
 
+// ---- compaction of the probe sink's hit bits (izg_decode_intersect) -----
+// Bit i of `hits` is set when s[i] was found in a decoded tile.  Equal
+// elements of s are either all found or none (a value's repeats are merged
+// in the same round or the next), so repeats are dropped by keeping bit i
+// only when bit i-1 is clear or s[i-1] != s[i].  One warp per group of 32
+// hit words (1,024 elements of s), lane j on element j of each word; loads
+// of s are coalesced and issued only for set bits.
+
+constexpr int kGroupWords = 32;
+
+// Calls f(keep_mask, x) for the group's words in order; x = s[32w+lane]
+// when this lane's bit is set.  The loads of 8 words are issued together;
+// lane 0's predecessor is lane 31 of the previous word (loaded whenever
+// both bits are set, which is the only case the comparison needs it).
+template <typename F>
+__device__ __forceinline__ void for_group(const uint32_t* __restrict__ s,
+                                          const uint32_t* __restrict__ hits, uint64_t nw,
+                                          uint64_t g, F&& f) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = g * kGroupWords;
+  const uint32_t mw = w0 + lane < nw ? hits[w0 + lane] : 0u;
+  uint32_t prev_m = w0 ? hits[w0 - 1] : 0u;  // previous group's last word
+  uint32_t prev_x = (prev_m >> 31) && lane == 31 ? __ldg(s + 32 * w0 - 1) : 0u;
+#pragma unroll 1
+  for (int k0 = 0; k0 < kGroupWords; k0 += 8) {
+    uint32_t ms[8], xs[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      ms[t] = __shfl_sync(0xFFFFFFFFu, mw, k0 + t);
+      xs[t] = (ms[t] >> lane) & 1u ? __ldg(s + 32 * (w0 + k0 + t) + lane) : 0u;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const uint32_t m = ms[t], x = xs[t];
+      if (m) {
+        const bool bit = (m >> lane) & 1u;
+        const bool pbit = lane ? (m >> (lane - 1)) & 1u : prev_m >> 31;
+        uint32_t px = __shfl_up_sync(0xFFFFFFFFu, x, 1);
+        const uint32_t carry = __shfl_sync(0xFFFFFFFFu, prev_x, 31);
+        if (lane == 0) px = carry;
+        f(__ballot_sync(0xFFFFFFFFu, bit && !(pbit && px == x)), x);
+      }
+      prev_m = m;
+      prev_x = x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    hits_count(const uint32_t* __restrict__ s, const uint32_t* __restrict__ hits, uint64_t nw,
+               uint64_t ngroups, uint32_t* __restrict__ group_count) {
+  const uint64_t g = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (g >= ngroups) return;
+  uint32_t total = 0;
+  for_group(s, hits, nw, g, [&](uint32_t keep, uint32_t) { total += __popc(keep); });
+  if ((threadIdx.x & 31) == 0) group_count[g] = total;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    hits_write(const uint32_t* __restrict__ s, const uint32_t* __restrict__ hits, uint64_t nw,
+               uint64_t ngroups, const uint32_t* __restrict__ group_off,
+               uint32_t* __restrict__ out) {
+  const uint64_t g = (uint64_t)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+  if (g >= ngroups) return;
+  const int lane = threadIdx.x & 31;
+  uint32_t o = group_off[g];
+  for_group(s, hits, nw, g, [&](uint32_t keep, uint32_t x) {
+    if ((keep >> lane) & 1u) out[o + __popc(keep & ((1u << lane) - 1u))] = x;
+    o += __popc(keep);
+  });
+}
+
 }  // namespace
+
+// Words of hit bits for a probe list of n_s (one spare word: a round's
+// ballot may straddle two words) and compaction groups.
+uint64_t hit_words(uint64_t n_s) { return (n_s + 31) / 32 + 1; }
+uint64_t compact_tiles(uint64_t n_s) { return ((n_s + 31) / 32 + kGroupWords - 1) / kGroupWords; }
+
+int compact_hits(const uint32_t* d_s, uint64_t n_s, const uint32_t* hits, uint32_t* groups,
+                 uint32_t* d_out, uint64_t* d_count, cudaStream_t st) {
+  if (n_s == 0)
+    return cudaMemsetAsync(d_count, 0, sizeof(uint64_t), st) == cudaSuccess ? IZG_SUCCESS
+                                                                           : IZG_ERR_CUDA;
+  const uint64_t nw = (n_s + 31) / 32, ng = compact_tiles(n_s);
+  const uint64_t grid = (ng + kThreads / 32 - 1) / (kThreads / 32);
+  if (ng > 0x7FFFFFFFu) return IZG_ERR_INVALID_ARGUMENT;
+  hits_count<<<(unsigned)grid, kThreads, 0, st>>>(d_s, hits, nw, ng, groups);
+  isect_scan<<<1, kThreads, 0, st>>>(groups, (uint32_t)ng, d_count);
+  hits_write<<<(unsigned)grid, kThreads, 0, st>>>(d_s, hits, nw, ng, groups, d_out);
+  return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+}
+
 }  // namespace izg
 
 extern "C" uint64_t izg_intersect_workspace_size(uint64_t n_a, uint64_t n_b) {

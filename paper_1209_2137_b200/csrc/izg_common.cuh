@@ -264,10 +264,18 @@ __device__ __forceinline__ void store_direct(const uint32_t (&v)[4][4], uint32_t
 // bank groups), then one TMA tensor store writes 16 full 128-byte rows.
 // Two tiles per warp alternate; a tile is reused once its store has read it.
 struct OutStage {
+  static constexpr bool kProbe = false;  // see ProbeStage (probe.cuh)
   uint32_t base;     // shared address of the warp's two tiles (1024-aligned)
   uint32_t buf;
   const void* tmap;  // 2-D map of the output: rows of 32 integers, box 16 rows
   bool leader;
+
+  __device__ __forceinline__ void begin_chunk() {}
+  // Iterations that do not take the TMA path (short tails, unaligned output).
+  __device__ __forceinline__ void direct(const uint32_t (&v)[4][4], uint32_t* o, bool oal,
+                                         bool live, uint32_t /*nvalid*/, int /*lane*/) {
+    if (live) store_direct(v, o, oal);
+  }
 
   __device__ __forceinline__ void put(const uint32_t (&v)[4][4], int lane, uint32_t row) {
     if (leader) bulk_wait_read<1>();
@@ -335,6 +343,7 @@ struct OutStage {
 // integers), decoded by one lane straight from global memory and continued
 // through the prefix sum from `carry` (codec.cpp:56-66).  Returns an
 // izg_status; *rem_bytes = bytes consumed.
+// `out` is the chunk's output (integer `core + i` goes to out[core + i]).
 template <int DELTA>
 __device__ int32_t vbyte_tail(const uint8_t* bytes, uint32_t nbytes, uint32_t core,
                               uint32_t count, uint4 carry, uint32_t* out, uint32_t* rem_bytes) {

@@ -16,10 +16,11 @@ class DeviceBatch:
 
     indexed=True gives SIMD-FastPFOR batches a decode workspace, so decode()
     runs izg_decode_ws's two-launch path (page index pass + table-driven
-    decode); indexed=False keeps the single fused launch of izg_decode."""
+    decode); indexed=False keeps the single fused launch of izg_decode.
+    materialize=False allocates no output (for decode_intersect_device)."""
 
     def __init__(self, codec: Codec, enc: Encoded, device=None, *, raw: bool = False,
-                 out=None, indexed: bool = True):
+                 out=None, indexed: bool = True, materialize: bool = True):
         import torch
 
         self.torch = torch
@@ -31,7 +32,9 @@ class DeviceBatch:
         self.payload_words = enc.payload_words
         self.words = torch.from_numpy(enc.words.view(np.int32)).to(self.device)
         self.table = torch.from_numpy(enc.table.view(np.uint8)).to(self.device)
-        if out is not None:
+        if not materialize:  # decode_intersect_device only: no output buffer
+            self.out = torch.empty(1, dtype=torch.int32, device=self.device)
+        elif out is not None:
             assert out.numel() >= self.n_out and out.dtype == torch.int32
             self.out = out
         else:
@@ -161,9 +164,47 @@ def intersect_device(a, b, stream=None):
     return out[:int(count.item())]
 
 
-def intersect(codec: Codec, enc_a: Encoded, enc_b: Encoded, device=None) -> np.ndarray:
+def decode_intersect_device(batch: "DeviceBatch", s_list, stream=None):
+    """Fused decode -> intersect (izg_decode_intersect): decodes `batch`'s
+    chunks and intersects them with the nondecreasing CUDA tensor `s_list`
+    without writing the decoded integers anywhere (each tile is merged
+    against s_list in shared memory).  Returns a CUDA tensor of the distinct
+    common values, ascending; per-chunk statuses land in batch.status."""
+    import torch
+
+    dev = s_list.device
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    L = N.lib()
+    ns = s_list.numel()
+    out = torch.empty(max(ns, 1), dtype=torch.int32, device=dev)
+    count = torch.zeros(1, dtype=torch.int64, device=dev)
+    ws = torch.empty(L.izg_decode_intersect_workspace_size(ns), dtype=torch.uint8, device=dev)
+    rc = L.izg_decode_intersect(batch.codec.codec, batch.delta, N.ptr(batch.words),
+                                N.ptr(batch.table), batch.n_chunks,
+                                N.ptr(s_list) if ns else None, ns, N.ptr(out), N.ptr(count),
+                                N.ptr(batch.status), N.ptr(ws), ws.numel(), s.cuda_stream)
+    if rc != N.SUCCESS:
+        raise RuntimeError(f"izg_decode_intersect failed: {rc}")
+    return out[:int(count.item())]
+
+
+def intersect(codec: Codec, enc_a: Encoded, enc_b: Encoded, device=None,
+              fused: bool = True) -> np.ndarray:
     """Decode two encoded arrays (posting lists) on the GPU and intersect them
-    there; only the intersection is copied back (numpy.intersect1d result)."""
+    there; only the intersection is copied back (numpy.intersect1d result).
+
+    fused=True (default): the shorter list is decoded to HBM and the longer
+    one goes through izg_decode_intersect, so it is never materialised.
+    fused=False: both are decoded, then izg_intersect_sorted."""
+    if fused:
+        short, long_ = (enc_a, enc_b) if enc_a.n_out <= enc_b.n_out else (enc_b, enc_a)
+        bs = DeviceBatch(codec, short, device)
+        bl = DeviceBatch(codec, long_, device, materialize=False, indexed=False)
+        bs.decode()
+        bs.check()
+        r = decode_intersect_device(bl, bs.out[:bs.n_out])
+        bl.check()
+        return r.cpu().numpy().view(np.uint32)
     ba = DeviceBatch(codec, enc_a, device)
     bb = DeviceBatch(codec, enc_b, device)
     ba.decode()
