@@ -120,6 +120,9 @@ typedef enum izg_status {
   IZG_E_BP32_TRUNC_PAYLOAD = 36, /* codec_binpack.cpp:52-53 bp32: truncated payload  */
   /* SimplePFOR exception highs, codec_basic.cpp */
   IZG_E_S8_EXHAUSTED = 37,     /* codec_basic.cpp:302-303 simple8b: stream exhausted before count */
+  /* internal: the split decode's look-back made no progress (a bug, never
+     a property of the input; reported instead of hanging the device) */
+  IZG_E_SPLIT_STALL = 38,
   /* misuse -> std::invalid_argument */
   IZG_E_COUNT_MULTIPLE = 64,   /* codec_binpack.cpp:13-14, codec_patched.cpp:53-54 count % 128 != 0 */
   IZG_E_PAGE_TOO_LARGE = 65,   /* codec_patched.cpp:55-56 page exceeds 65536 integers */
@@ -172,17 +175,27 @@ int izg_decode(int codec, int delta, const uint32_t* d_words,
                int32_t* d_status, uint32_t* d_consumed, void* stream);
 
 /* Bytes of device workspace izg_decode_ws can use for n_chunks chunks of
- * this codec (0 when the codec has no indexed path: SIMD-BP128). */
+ * this codec.  SIMD-FastPFOR: the page index (a two-launch index pass +
+ * table-driven decode).  Small batches of SIMD-BP128 or SIMD-FastPFOR add
+ * the split decode's look-back state (several warps per chunk, decoupled
+ * look-back carry; IZG_SPLIT=0/1 in the environment forces it off/on).
+ * 0 when nothing applies. */
 uint64_t izg_decode_workspace_size(int codec, uint32_t n_chunks);
+
+/* The page index alone (SIMD-FastPFOR; 0 otherwise): a workspace of exactly
+ * this size selects the one-warp-per-page indexed decode even for small
+ * batches. */
+uint64_t izg_decode_index_workspace_size(int codec, uint32_t n_chunks);
 
 /* izg_decode with a caller-owned device workspace (16-byte aligned, at least
  * izg_decode_workspace_size bytes; otherwise this is exactly izg_decode).
  * SIMD-FastPFOR then runs as two stream-ordered launches: a page index pass
- * (one thread per page walks the byte array and the exception directory and
- * makes every metadata check of codec_patched.cpp:292-416) and the fused
- * decode reading per-block records.  Results and statuses are identical to
- * izg_decode's; the workspace must stay untouched until the decode completes
- * on `stream`. */
+ * (one warp per page parses the byte array and the exception directory and
+ * makes every metadata check of codec_patched.cpp:292-416) and the decode
+ * reading per-block records.  Small batches run the split decode (several
+ * warps per chunk with a decoupled look-back carry).  Results and statuses
+ * are identical to izg_decode's; the workspace must stay untouched until the
+ * decode completes on `stream`. */
 int izg_decode_ws(int codec, int delta, const uint32_t* d_words,
                   const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
                   int32_t* d_status, uint32_t* d_consumed, void* d_workspace,

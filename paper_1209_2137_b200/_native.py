@@ -60,6 +60,8 @@ def lib() -> C.CDLL:
                                 C.c_uint64, vp]
     L.izg_decode_workspace_size.restype = C.c_uint64
     L.izg_decode_workspace_size.argtypes = [C.c_int, C.c_uint32]
+    L.izg_decode_index_workspace_size.restype = C.c_uint64
+    L.izg_decode_index_workspace_size.argtypes = [C.c_int, C.c_uint32]
     L.izg_container_scan.restype = C.c_int
     L.izg_container_scan.argtypes = [vp, C.c_uint64, C.c_int, vp, vp]
     L.izg_container_index.restype = C.c_int
@@ -107,7 +109,8 @@ def lib() -> C.CDLL:
 
 # Symbols include/intzip_b200.h declares (checked by the CPU test suite).
 ABI_SYMBOLS = ("izg_status_string", "izg_parse_codec_name", "izg_layout_chunks",
-               "izg_decode", "izg_decode_ws", "izg_decode_workspace_size", "izg_checksum", "izg_decode_host", "izg_release_host_scratch",
+               "izg_decode", "izg_decode_ws", "izg_decode_workspace_size",
+               "izg_decode_index_workspace_size", "izg_checksum", "izg_decode_host", "izg_release_host_scratch",
                "izg_encode", "izg_encode_bound", "izg_container_scan", "izg_container_index",
                "izg_container_decode_host", "izg_intersect_workspace_size",
                "izg_intersect_sorted", "izg_decode_intersect_workspace_size",

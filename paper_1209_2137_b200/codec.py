@@ -24,6 +24,9 @@ DELTA_NAMES = {N.DELTA_NONE: "none", N.DELTA_D1: "scalar", N.DELTA_D4: "stride4"
                N.DELTA_D2: "stride2(ext)", N.DELTA_DM: "max4(ext)"}
 
 
+SPLIT_STALL = 38  # IZG_E_SPLIT_STALL
+
+
 class CorruptError(RuntimeError):
     """intzip::CorruptError (errors.h:8-14): malformed compressed input."""
 
@@ -39,6 +42,8 @@ def raise_for_status(status: int, chunk: int | None = None) -> None:
         return
     if status >= 64:  # std::invalid_argument sites
         raise ValueError(N.status_string(status))
+    if status == SPLIT_STALL:  # internal error of the split decode, not the input
+        raise RuntimeError(N.status_string(status))
     raise CorruptError(status, chunk)
 
 

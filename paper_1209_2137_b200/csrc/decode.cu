@@ -16,6 +16,7 @@
 
 #include "../../include/intzip_b200.h"
 #include "decode_kernel.cuh"
+#include "split.cuh"
 #include "encode.cuh"
 
 namespace izg {
@@ -79,6 +80,35 @@ bool make_out_map(CUtensorMap* m, uint32_t* out) {
 KernelFn pick_fastpfor_scalar(int delta);
 // Probe-sink (decode -> intersect) kernels: decode_probe.cu.
 KernelFn pick_probe_kernel(int codec, int delta);
+// Split (several warps per chunk) kernels: decode_split.cu.
+using SplitFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
+                         uint32_t*, SplitArgs, IdxView);
+SplitFn pick_split(int codec, int delta);
+
+// Small batches decode with the split kernel (split.cuh) when the caller
+// gives a workspace: with few chunks one warp per chunk leaves SMs idle.
+// Crossovers measured with tools/split_sweep.py on B200 (65,536-integer
+// chunks): SIMD-BP128 wins up to ~512 chunks (64: 0.072 vs 0.114 ms),
+// SIMD-FastPFOR up to ~1,024 pages (64: 0.157 vs 0.384 ms; 1,024: 0.415 vs
+// 0.504 ms).  IZG_SPLIT=0 / 1 in the environment forces it off / on.
+constexpr uint32_t kSplitMaxChunksBp = 512, kSplitMaxChunksFp = 1024;
+bool split_wanted(int codec, uint32_t n_chunks) {
+  if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return false;
+  static const int force = [] {
+    const char* e = std::getenv("IZG_SPLIT");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (force >= 0) return force != 0;
+  return n_chunks <= (codec == IZG_SIMDBP128 ? kSplitMaxChunksBp : kSplitMaxChunksFp);
+}
+uint64_t split_ws_offset(int codec, uint32_t n_chunks) {
+  return codec == IZG_SIMDFASTPFOR ? (idx_workspace_bytes(n_chunks) + 15) / 16 * 16 : 0;
+}
+uint64_t workspace_bytes(int codec, uint32_t n_chunks) {
+  const uint64_t base = codec == IZG_SIMDFASTPFOR ? idx_workspace_bytes(n_chunks) : 0;
+  if (!split_wanted(codec, n_chunks)) return base;
+  return split_ws_offset(codec, n_chunks) + split_state_bytes(n_chunks);
+}
 
 
 constexpr uint32_t kCounterSlots = 1024;
@@ -90,8 +120,9 @@ struct DeviceInfo {
   bool init = false;
   bool ok = false;
   int sms = 0;
-  // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink)][delta]
-  int occ[3 * kCodecs][5] = {};
+  // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink,
+  //  + 3 kCodecs: split kernels)][delta]
+  int occ[4 * kCodecs][5] = {};
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -111,8 +142,8 @@ int device_of(const void* p) {
 }
 
 // `variant` = codec, + kCodecs for the indexed page decode kernels, + 2 kCodecs
-// for the probe-sink kernels.
-int prepare(int dev, int variant, int delta, KernelFn fn, int threads, size_t smem,
+// for the probe-sink kernels, + 3 kCodecs for the split kernels.
+int prepare(int dev, int variant, int delta, const void* fn, int threads, size_t smem,
             int* grid_per_sm, int* sms, uint32_t** counter) {
   if (dev < 0 || dev >= 64) return IZG_ERR_INVALID_ARGUMENT;
   std::lock_guard<std::mutex> lk(g_dev_mu);
@@ -208,7 +239,13 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   const size_t smem = idx     ? Layout<IZG_SIMDFASTPFOR, true>::kSmem
                       : paged ? Layout<IZG_SIMDFASTPFOR>::kSmem
                               : Layout<IZG_SIMDBP128>::kSmem;
-  int rc = prepare(dev, codec + (idx ? kCodecs : probe ? 2 * kCodecs : 0), delta, fn, warps * 32, smem, &per_sm, &sms,
+  const bool split = !probe && split_wanted(codec, n_chunks) && d_ws &&
+                     (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
+                     ws_bytes >= workspace_bytes(codec, n_chunks);
+  const void* kfn = split ? reinterpret_cast<const void*>(pick_split(codec, delta))
+                          : reinterpret_cast<const void*>(fn);
+  int rc = prepare(dev, codec + (split ? 3 * kCodecs : idx ? kCodecs : probe ? 2 * kCodecs : 0),
+                   delta, kfn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -229,9 +266,23 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                                         : fp_index_kernel<true, kVertical>;
     ifn<<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks, n_chunks, ix);
   }
+  if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
+  if (split) {
+    SplitArgs sa;
+    sa.seg = reinterpret_cast<SegState*>(static_cast<uint8_t*>(d_ws) +
+                                         split_ws_offset(codec, n_chunks));
+    sa.next_unit = counter;
+    if (cudaMemsetAsync(sa.seg, 0, split_state_bytes(n_chunks), s) != cudaSuccess)
+      return IZG_ERR_CUDA;
+    const uint64_t units = (uint64_t)n_chunks * kMaxSegs;
+    const uint32_t grid =
+        (uint32_t)std::min<uint64_t>((units + warps - 1) / warps, (uint64_t)per_sm * sms);
+    pick_split(codec, delta)<<<grid, warps * 32, smem, s>>>(d_words, d_chunks, n_chunks, d_out,
+                                                             d_status, d_consumed, sa, ix);
+    return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+  }
   const uint64_t want = (n_chunks + warps - 1) / warps;
   const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
-  if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
   CUtensorMap omap;
   std::memset(&omap, 0, sizeof(omap));
   const int tma_out = !probe && make_out_map(&omap, d_out) ? 1 : 0;
@@ -287,6 +338,10 @@ extern "C" int izg_decode_intersect(int codec, int delta, const uint32_t* d_word
 }
 
 extern "C" uint64_t izg_decode_workspace_size(int codec, uint32_t n_chunks) {
+  return izg::workspace_bytes(codec, n_chunks);
+}
+
+extern "C" uint64_t izg_decode_index_workspace_size(int codec, uint32_t n_chunks) {
   return codec == IZG_SIMDFASTPFOR ? izg::idx_workspace_bytes(n_chunks) : 0;
 }
 

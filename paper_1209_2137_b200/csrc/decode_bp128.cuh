@@ -262,14 +262,17 @@ __device__ int32_t bp32_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks,
 // Returns an izg_status; on success *pos_out = payload words consumed.
 // `orow` is the chunk's first output row (32 integers) for the TMA path, or
 // -1 when the output is not 128-byte aligned (direct stores then).
+// Split decode (split.cuh): blocks [blk_begin, nblocks) only, blk_begin a
+// multiple of 16 with the ring and `nw` starting at its meta-block; output
+// indices stay chunk-relative.
 template <int DELTA, bool ALIGNED, typename OS>
 __device__ int32_t bp128_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks,
                               uint32_t* out, bool out_aligned, int64_t orow, uint4& carry,
-                              uint32_t* pos_out) {
+                              uint32_t* pos_out, uint32_t blk_begin = 0) {
   const int lane = threadIdx.x & 31;
   const uint32_t q = lane >> 3, s8 = lane & 7;
   uint32_t pos = 0;
-  for (uint32_t mb0 = 0; mb0 < nblocks; mb0 += 16) {
+  for (uint32_t mb0 = blk_begin; mb0 < nblocks; mb0 += 16) {
     const uint32_t groups = min(16u, nblocks - mb0);
     if (pos + 4 > nw) return IZG_E_BP_TRUNC_DESC;
     r.release_below(4u * pos);

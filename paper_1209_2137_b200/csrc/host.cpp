@@ -52,6 +52,7 @@ extern "C" const char* izg_status_string(int32_t s) {
     case IZG_E_BP32_WIDTH: return "bp32: width byte exceeds 32";
     case IZG_E_BP32_TRUNC_PAYLOAD: return "bp32: truncated payload";
     case IZG_E_S8_EXHAUSTED: return "simple8b: stream exhausted before count";
+    case IZG_E_SPLIT_STALL: return "internal: split decode look-back stalled";
     case IZG_E_COUNT_MULTIPLE: return "count must be a multiple of 128";
     case IZG_E_PAGE_TOO_LARGE: return "patched codec: page exceeds 65536 integers";
     case IZG_E_DECREASING: return "delta encode: input is not nondecreasing";

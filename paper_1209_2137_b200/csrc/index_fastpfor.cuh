@@ -202,7 +202,7 @@ static __device__ bool fp_positions_bad_idx(const uint4* rec, const uint8_t* ba,
 template <int DELTA, int ST, typename OS>
 __device__ bool fp_blocks_idx(WarpRing& r, OS& os, const uint32_t* dir_base, const uint4* rec,
                               const uint32_t* page, uint32_t A, uint32_t nblocks, uint32_t* out,
-                              bool oal, int64_t orow, uint4& carry) {
+                              bool oal, int64_t orow, uint4& carry, uint32_t wbase = 1) {
   const int lane = threadIdx.x & 31;
   const uint32_t q = lane >> 3, s8 = lane & 7;
   const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
@@ -223,15 +223,15 @@ __device__ bool fp_blocks_idx(WarpRing& r, OS& os, const uint32_t* dir_base, con
     const bool tot = __any_sync(0xFFFFFFFFu, myc != 0);
 
     // Stream window: packed words [first, after) (the stream starts at word 1).
-    r.release_below(4u * (first - 1));
-    r.ensure(4u * (after - 1));
+    r.release_below(4u * (first - wbase));
+    r.ensure(4u * (after - wbase));
     uint32_t v[4][4];
     if (ST != kVertical)
-      unpack_scalar_slots(r, myoff - 1, myb, s8, v);
+      unpack_scalar_slots(r, myoff - wbase, myb, s8, v);
     else if (r.phase == 0)
-      unpack_slots_aligned(r, r.ring_off() + 4u * (myoff - 1), myb, s8, v);
+      unpack_slots_aligned(r, r.ring_off() + 4u * (myoff - wbase), myb, s8, v);
     else
-      unpack_slots_unaligned(r, myoff - 1, myb, s8, v);
+      unpack_slots_unaligned(r, myoff - wbase, myb, s8, v);
     if (tot) {
       const uint32_t mybase = dir_base[myw];
       const uint32_t t = os.acquire();
@@ -257,6 +257,9 @@ __device__ bool fp_blocks_idx(WarpRing& r, OS& os, const uint32_t* dir_base, con
   }
   return __any_sync(0xFFFFFFFFu, bad);
 }
+
+// Blocks of one page from its records `rec` (split.cuh passes a range:
+// `wbase` = page word the ring starts at, 1 for a whole page).
 
 // Whole indexed page `c` (record written by fp_index_kernel); same contract
 // as fastpfor_core.

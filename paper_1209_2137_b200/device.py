@@ -17,10 +17,13 @@ class DeviceBatch:
     indexed=True gives SIMD-FastPFOR batches a decode workspace, so decode()
     runs izg_decode_ws's two-launch path (page index pass + table-driven
     decode); indexed=False keeps the single fused launch of izg_decode.
-    materialize=False allocates no output (for decode_intersect_device)."""
+    materialize=False allocates no output (for decode_intersect_device).
+    split=False sizes the workspace for the page index only, so small batches
+    keep one warp per chunk instead of the split kernel (csrc/split.cuh)."""
 
     def __init__(self, codec: Codec, enc: Encoded, device=None, *, raw: bool = False,
-                 out=None, indexed: bool = True, materialize: bool = True):
+                 out=None, indexed: bool = True, materialize: bool = True,
+                 split: bool = True):
         import torch
 
         self.torch = torch
@@ -44,7 +47,11 @@ class DeviceBatch:
         self.consumed = torch.zeros(max(self.n_chunks, 1), dtype=torch.int32,
                                     device=self.device)
         self.sums = torch.zeros(2, dtype=torch.int64, device=self.device)
-        ws = N.lib().izg_decode_workspace_size(codec.codec, self.n_chunks) if indexed else 0
+        L = N.lib()
+        ws = 0
+        if indexed:
+            ws = (L.izg_decode_workspace_size(codec.codec, self.n_chunks) if split
+                  else L.izg_decode_index_workspace_size(codec.codec, self.n_chunks))
         self.workspace = (torch.empty(ws, dtype=torch.uint8, device=self.device)
                           if ws else None)
 

@@ -99,13 +99,23 @@ def corpus(name, seed):
 
 
 def both_paths(codec, enc, raw=False):
+    """(fused one-warp, workspace path) results; the workspace path of a small
+    batch is the split kernel, and the one-warp indexed kernel (workspace of
+    the page index only) must agree with both."""
     res = []
-    for indexed in (False, True):
-        b = P.DeviceBatch(codec, enc, raw=raw, indexed=indexed)
+    for indexed, split in ((False, True), (True, False), (True, True)):
+        b = P.DeviceBatch(codec, enc, raw=raw, indexed=indexed, split=split)
         assert (b.workspace is not None) == indexed
         b.decode()
         res.append((b.statuses(), b.output(), b.consumed[:b.n_chunks].cpu().numpy()))
-    return res
+    (s0, o0, u0), (s1, o1, u1), (s2, o2, u2) = res
+    assert np.array_equal(s0, s1) and np.array_equal(s1, s2)
+    assert np.array_equal(u1, u2)
+    for i in np.nonzero(s1 == 0)[0]:
+        a = int(enc.table["out_off"][i])
+        n = int(enc.table["n"][i])
+        assert np.array_equal(o1[a:a + n], o2[a:a + n]), i
+    return res[0], res[2]
 
 
 @pytest.mark.parametrize("name", FP_NAMES)
@@ -199,5 +209,9 @@ def test_workspace_too_small_falls_back_to_fused(cuda):
     assert rc == N.SUCCESS
     b.check()
     assert np.array_equal(b.output(), arr)
-    assert N.lib().izg_decode_workspace_size(0, 100) == 0
-    assert N.lib().izg_decode_workspace_size(1, 100) == 100 * (16 + 128 + 512 * 16)
+    # large batches: the page index only (SIMD-FastPFOR), nothing for SIMD-BP128;
+    # small ones add the split kernel's look-back state (test_gpu_split.py)
+    n = 1 << 14
+    assert N.lib().izg_decode_workspace_size(0, n) == 0
+    assert N.lib().izg_decode_workspace_size(1, n) == n * (16 + 128 + 512 * 16)
+    assert N.lib().izg_decode_workspace_size(1, 100) > 100 * (16 + 128 + 512 * 16)
