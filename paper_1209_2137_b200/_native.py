@@ -11,7 +11,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libintzip_b200.so")
+# IZG_LIB_PATH: developer A/B runs of alternative builds (tools/); the default
+# is the in-tree build.
+LIB_PATH = os.environ.get("IZG_LIB_PATH") or os.path.join(_HERE, "_lib", "libintzip_b200.so")
 
 # izg_chunk (include/intzip_b200.h): 24 bytes, naturally aligned.
 CHUNK_DTYPE = np.dtype([("word_off", "<u8"), ("n_words", "<u4"), ("n", "<u4"),

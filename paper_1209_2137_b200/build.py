@@ -18,6 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libintzip_b200.so")
+OBJDIR = os.path.join(LIBDIR, "obj")
 
 SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "decode_split.cu", "intersect.cu", "host.cpp", "host_encode.cpp",
            "host_datagen.cpp", "container.cpp"]
@@ -47,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(LIBDIR, exist_ok=True)
     if not force and not _stale(LIB, _deps()):
         return LIB
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = OBJDIR
     os.makedirs(objdir, exist_ok=True)
     extra = os.environ.get("IZG_NVCC_EXTRA", "").split()  # debug builds only
 
