@@ -88,9 +88,10 @@ SplitFn pick_split(int codec, int delta);
 // Small batches decode with the split kernel (split.cuh) when the caller
 // gives a workspace: with few chunks one warp per chunk leaves SMs idle.
 // Crossovers measured with tools/split_sweep.py on B200 (65,536-integer
-// chunks): SIMD-BP128 wins up to ~512 chunks (64: 0.072 vs 0.114 ms),
-// SIMD-FastPFOR up to ~1,024 pages (64: 0.157 vs 0.384 ms; 1,024: 0.415 vs
-// 0.504 ms).  IZG_SPLIT=0 / 1 in the environment forces it off / on.
+// chunks): SIMD-BP128 wins up to ~512 chunks (64: 0.035 vs 0.113 ms; 512:
+// 0.101 vs 0.114; 1,024: 0.145 vs 0.115), SIMD-FastPFOR up to ~1,024 pages
+// (64: 0.154 vs 0.379 ms; 1,024: 0.398 vs 0.504 ms).  IZG_SPLIT=0 / 1 in the
+// environment forces it off / on.
 constexpr uint32_t kSplitMaxChunksBp = 512, kSplitMaxChunksFp = 1024;
 bool split_wanted(int codec, uint32_t n_chunks) {
   if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return false;
@@ -274,7 +275,18 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     sa.next_unit = counter;
     if (cudaMemsetAsync(sa.seg, 0, split_state_bytes(n_chunks), s) != cudaSuccess)
       return IZG_ERR_CUDA;
-    const uint64_t units = (uint64_t)n_chunks * kMaxSegs;
+    // SIMD-BP128 sizes segments to the batch; SIMD-FastPFOR keeps the
+    // smallest (measured best at every batch size it is selected for)
+    sa.seg_blocks = codec == IZG_SIMDBP128
+                        ? split_seg_blocks(n_chunks, (uint32_t)(per_sm * sms * warps))
+                        : kSegBlocks;
+    static const int force_segs = [] {  // IZG_SPLIT_SEGS=1..16: tuning sweeps
+      const char* e = std::getenv("IZG_SPLIT_SEGS");
+      const int v = e ? std::atoi(e) : 0;
+      return v >= 1 && v <= (int)kMaxSegs && (v & (v - 1)) == 0 ? v : 0;
+    }();
+    if (force_segs) sa.seg_blocks = (IZG_CHUNK_SIZE / 128) / force_segs;
+    const uint64_t units = (uint64_t)n_chunks * ((IZG_CHUNK_SIZE / 128) / sa.seg_blocks);
     const uint32_t grid =
         (uint32_t)std::min<uint64_t>((units + warps - 1) / warps, (uint64_t)per_sm * sms);
     pick_split(codec, delta)<<<grid, warps * 32, smem, s>>>(d_words, d_chunks, n_chunks, d_out,

@@ -265,6 +265,26 @@ __device__ int32_t bp32_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks,
 // Split decode (split.cuh): blocks [blk_begin, nblocks) only, blk_begin a
 // multiple of 16 with the ring and `nw` starting at its meta-block; output
 // indices stay chunk-relative.
+// OS::kAgg (AggStage, split.cuh): nothing is written; the deltas are only
+// summed per carry component, and `carry` is advanced by the segment's
+// aggregate (what the scan would have carried out of it).
+template <int DELTA>
+__device__ __forceinline__ void accumulate(const uint32_t (&v)[4][4], uint4& a) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (DELTA == IZG_DELTA_D4) {
+      a.x += v[c][0]; a.y += v[c][1]; a.z += v[c][2]; a.w += v[c][3];
+    } else if (DELTA == IZG_DELTA_D1) {
+      a.x += v[c][0] + v[c][1] + v[c][2] + v[c][3];
+    } else if (DELTA == IZG_DELTA_D2) {
+      a.x += v[c][0] + v[c][2];
+      a.y += v[c][1] + v[c][3];
+    } else if (DELTA == IZG_DELTA_DM) {
+      a.x += v[c][3];  // DM carries the last value of each 4-vector
+    }
+  }
+}
+
 template <int DELTA, bool ALIGNED, typename OS>
 __device__ int32_t bp128_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks,
                               uint32_t* out, bool out_aligned, int64_t orow, uint4& carry,
@@ -272,6 +292,7 @@ __device__ int32_t bp128_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks
   const int lane = threadIdx.x & 31;
   const uint32_t q = lane >> 3, s8 = lane & 7;
   uint32_t pos = 0;
+  uint4 acc = make_uint4(0, 0, 0, 0);  // OS::kAgg: this lane's sums
   for (uint32_t mb0 = blk_begin; mb0 < nblocks; mb0 += 16) {
     const uint32_t groups = min(16u, nblocks - mb0);
     if (pos + 4 > nw) return IZG_E_BP_TRUNC_DESC;
@@ -298,6 +319,10 @@ __device__ int32_t bp128_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks
         unpack_slots_aligned(r, r.ring_off() + 4u * (pay + excl), width, s8, v);
       else
         unpack_slots_unaligned(r, pay + excl, width, s8, v);
+      if constexpr (OS::kAgg) {
+        accumulate<DELTA>(v, acc);
+        continue;
+      }
       scan<DELTA>(v, carry, lane);
       if (orow >= 0 && g0 + 4 <= groups) {
         os.put(v, lane, (uint32_t)(orow + 4 * (mb0 + g0)));
@@ -307,6 +332,19 @@ __device__ int32_t bp128_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks
       }
     }
     pos = pay + m.size;
+  }
+  if constexpr (OS::kAgg) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {
+      acc.x += __shfl_xor_sync(0xFFFFFFFFu, acc.x, d);
+      if (DELTA == IZG_DELTA_D4 || DELTA == IZG_DELTA_D2)
+        acc.y += __shfl_xor_sync(0xFFFFFFFFu, acc.y, d);
+      if (DELTA == IZG_DELTA_D4) {
+        acc.z += __shfl_xor_sync(0xFFFFFFFFu, acc.z, d);
+        acc.w += __shfl_xor_sync(0xFFFFFFFFu, acc.w, d);
+      }
+    }
+    carry = u4add(carry, acc);
   }
   *pos_out = pos;
   return IZG_OK;

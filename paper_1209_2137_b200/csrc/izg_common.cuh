@@ -265,6 +265,7 @@ __device__ __forceinline__ void store_direct(const uint32_t (&v)[4][4], uint32_t
 // Two tiles per warp alternate; a tile is reused once its store has read it.
 struct OutStage {
   static constexpr bool kProbe = false;  // see ProbeStage (probe.cuh)
+  static constexpr bool kAgg = false;    // see AggStage (split.cuh)
   uint32_t base;     // shared address of the warp's two tiles (1024-aligned)
   uint32_t buf;
   const void* tmap;  // 2-D map of the output: rows of 32 integers, box 16 rows

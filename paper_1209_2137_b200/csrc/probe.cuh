@@ -59,6 +59,7 @@ __device__ __forceinline__ uint32_t pick16(const uint32_t (&v)[4][4], uint32_t k
 
 struct ProbeStage {
   static constexpr bool kProbe = true;
+  static constexpr bool kAgg = false;
   uint32_t base;  // shared address of the warp's tile (FastPFOR patches there)
   bool leader;
   ProbeArgs pa;

@@ -13,21 +13,27 @@
 //  1. Start offset.  SIMD-FastPFOR (indexed): the page records of
 //     fp_index_kernel give every block's packed word, position byte and
 //     exception cursors directly.  SIMD-BP128: the meta-block descriptor
-//     chain (codec_binpack.cpp:96-117) is serial, so unit k waits for unit
-//     k-1 to publish its end offset, walks its own two descriptors (two
-//     dependent 16-byte loads, every reference check in order) and
-//     publishes its end offset before decoding anything.
-//  2. Decode with a zero carry (the same cores as the one-warp kernel),
-//     storing to HBM with plain stores so the lines stay in L2.
+//     chain (codec_binpack.cpp:96-117) is serial; every unit walks it from
+//     the chunk start itself (unit 0 first pulls the chunk into L2 with one
+//     bulk prefetch, so the hops are L2 hits), making every reference check
+//     in order on its own two descriptors.
+//  2. SIMD-BP128 array modes, reduce-then-scan: unless the predecessor's
+//     inclusive prefix is already out, one unpack pass sums the segment's
+//     deltas (no stores), the unit looks back (3.) and publishes its
+//     inclusive prefix, then decodes once with the true carry.  Otherwise
+//     (and for SIMD-FastPFOR): decode with a zero carry (the same cores as
+//     the one-warp kernel), storing to HBM with plain stores so the lines
+//     stay in L2.
 //  3. Decoupled look-back (Merrill & Garland's single-pass scan): publish the
 //     segment's aggregate (the local carry: last value per D4 lane class,
 //     etc.), then walk back over predecessors, adding aggregates until one
 //     publishes an inclusive prefix; publish this unit's inclusive prefix.
 //     The first error of the chunk in stream order travels with the
 //     prefixes.
-//  4. Fix-up: every lane re-reads exactly the integers it stored (L2 hits)
-//     and adds the exclusive prefix per residue class.  Skipped when the
-//     predecessor's inclusive prefix was already published at step 2.
+//  4. Fix-up (decode-first units only): every lane re-reads exactly the
+//     integers it stored (L2 hits) and adds the exclusive prefix per residue
+//     class.  Skipped when the predecessor's inclusive prefix was already
+//     published at step 2.
 // The last segment decodes the VByte remainder and writes the chunk's
 // status; an error on the BP128 offset chain stops the chunk's later units.
 // Spins are bounded (a broken chain reports IZG_E_SPLIT_STALL instead of
@@ -39,7 +45,10 @@
 
 namespace izg {
 
-constexpr uint32_t kSegBlocks = 32;  // 4,096 integers (2 BP128 meta-blocks)
+constexpr uint32_t kSegBlocks = 32;  // smallest segment: 4,096 integers (2 BP128 meta-blocks)
+#ifndef IZG_SPLIT_RTS
+#define IZG_SPLIT_RTS 1  // SIMD-BP128: reduce-then-scan instead of decode + fix-up
+#endif
 constexpr uint32_t kMaxSegs = IZG_CHUNK_SIZE / 128 / kSegBlocks;  // 16
 
 // Look-back state of one unit (80 bytes, zeroed before the launch).  Every
@@ -48,12 +57,10 @@ constexpr uint32_t kMaxSegs = IZG_CHUNK_SIZE / 128 / kSegBlocks;  // 16
 // and read with single-copy-atomic relaxed 64-bit accesses — no fences, so
 // publishing never waits for the unit's own output stores to drain.
 struct SegState {
-  uint32_t off;     // BP128: end offset + 1 (0 = not yet; kOffError = chain broken)
-  uint32_t pad[3];
+  uint32_t pad[4];
   unsigned long long agg[4];  // per residue class (scan()'s carry layout)
   unsigned long long pre[4];
 };
-constexpr uint32_t kOffError = 0xFFFFFFFFu;
 constexpr uint32_t kSpinLimit = 1u << 22;  // ~seconds of polling: a stall is a bug
 
 __host__ __device__ inline uint64_t split_state_bytes(uint32_t n_chunks) {
@@ -110,24 +117,12 @@ __device__ __forceinline__ bool try_read(const unsigned long long* w, uint32_t k
   return ok;
 }
 
-// Lane 0 only.  Spin until the offset word is set.
-__device__ __forceinline__ uint32_t spin_off(const uint32_t* p, bool* stalled) {
-  for (uint32_t i = 0;; ++i) {
-    const uint32_t v = ld_relaxed(p);
-    if (v) return v;
-    if (i >= kSpinLimit) {
-      *stalled = true;
-      return v;
-    }
-    if (i > 32) __nanosleep(64);
-  }
-}
-
 // Output sink of the split kernel: like OutStage but plain 16-byte stores
 // (no TMA: the fix-up re-reads each lane's own stores, which needs them in
 // the generic proxy and in L2).
 struct SegStage {
   static constexpr bool kProbe = false;
+  static constexpr bool kAgg = false;
   uint32_t base;  // the warp's shared tile (SIMD-FastPFOR patches there)
   uint32_t* out;  // chunk output (rows are chunk-relative)
   __device__ __forceinline__ void begin_chunk() {}
@@ -162,6 +157,16 @@ struct SegStage {
     }
   }
   __device__ __forceinline__ void drain() {}
+};
+
+// Sink of the aggregate pass (reduce-then-scan, SIMD-BP128): bp128_core
+// only sums the deltas; nothing reaches memory.
+struct AggStage {
+  static constexpr bool kProbe = false;
+  static constexpr bool kAgg = true;
+  __device__ __forceinline__ void put(const uint32_t (&)[4][4], int, uint32_t) {}
+  __device__ __forceinline__ void direct(const uint32_t (&)[4][4], uint32_t*, bool, bool,
+                                         uint32_t, int) {}
 };
 
 // Add the exclusive prefix P to the integers of blocks [b0, b1) (b0 a
@@ -257,7 +262,17 @@ __device__ __forceinline__ uint32_t bp_meta_words(const uint32_t* p, uint32_t po
 struct SplitArgs {
   SegState* seg;       // n_chunks * kMaxSegs states, zeroed
   uint32_t* next_unit;
+  uint32_t seg_blocks;  // blocks per segment: kSegBlocks << s (split_seg_blocks)
 };
+
+// Segment size for a batch: about four units per resident warp, so that
+// larger batches pay for fewer descriptor walks, look-backs and unit
+// start-ups (powers of two from 4,096 to 65,536 integers).
+__host__ __device__ inline uint32_t split_seg_blocks(uint32_t n_chunks, uint32_t warp_slots) {
+  uint32_t segs = kMaxSegs;
+  while (segs > 1 && (uint64_t)n_chunks * segs > 4ull * warp_slots) segs >>= 1;
+  return (IZG_CHUNK_SIZE / 128) / segs;
+}
 
 // Persistent split kernel: CODEC = IZG_SIMDBP128 or IZG_SIMDFASTPFOR
 // (indexed pages; fp_index_kernel ran first).  Array modes (DELTA != NONE)
@@ -294,15 +309,16 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
     if (lane == 0) u = atomicAdd(sa.next_unit, 1u);
     u = __shfl_sync(0xFFFFFFFFu, u, 0);
     const uint32_t k = u / n_chunks, c = u - k * n_chunks;
-    if (k >= kMaxSegs) break;
+    if (k >= (IZG_CHUNK_SIZE / 128) / sa.seg_blocks) break;
     const izg_chunk ch = chunks[c];
     const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
     const uint32_t nblocks = core / 128;
-    const uint32_t nseg = nblocks ? min((nblocks + kSegBlocks - 1) / kSegBlocks, kMaxSegs) : 1u;
+    const uint32_t SB = sa.seg_blocks;
+    const uint32_t nseg = nblocks ? (nblocks + SB - 1) / SB : 1u;
     if (k >= nseg) continue;
     const bool last = k == nseg - 1;
-    const uint32_t b0 = k * kSegBlocks;
-    const uint32_t b1 = last ? nblocks : b0 + kSegBlocks;
+    const uint32_t b0 = k * SB;
+    const uint32_t b1 = last ? nblocks : b0 + SB;
     SegState* const st = sa.seg + (size_t)c * kMaxSegs;
     int32_t err = precheck(CODEC, kArray, ch.n);
     if (err != IZG_OK) {  // every unit sees it; unit 0 reports
@@ -323,31 +339,36 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
     uint32_t pos0 = 0, pos_end = 0;
     uint4 hdr = make_uint4(0, 0, 0, 0);
     if (CODEC == IZG_SIMDBP128) {
+      // Every unit walks the descriptor chain from the chunk start itself
+      // (no waiting on its predecessor): unit 0 pulls the chunk into L2 and
+      // the other units' hops over earlier segments are L2 hits with a
+      // 4-lane size check; an error there belongs to an earlier unit, which
+      // reports it, so this unit just stops.
       int32_t werr = IZG_OK;
-      if (k > 0) {
-        if (lane == 0) {
-          const uint32_t v = spin_off(&st[k - 1].off, &stalled);
-          if (stalled) werr = IZG_E_SPLIT_STALL;
-          else if (v == kOffError) werr = -1;  // an earlier unit reported
-          else pos0 = v - 1;
+      if (k == 0 && lane == 0) prefetch_l2(p, 4u * ch.n_words);
+      uint32_t pos = 0;
+      for (uint32_t mb = 0; mb < b0; mb += 16) {
+        const bool fits = pos + 4 <= ch.n_words;
+        const uint32_t word = fits && lane < 4 ? __ldg(p + pos + lane) : 0u;
+        uint32_t sz = __dp4a(word, 0x01010101u, 0u);
+        sz += __shfl_xor_sync(0xFFFFFFFFu, sz, 1);
+        sz += __shfl_xor_sync(0xFFFFFFFFu, sz, 2);
+        sz = __shfl_sync(0xFFFFFFFFu, sz, 0);
+        const bool bad = !fits || __any_sync(0xFFFFFFFFu, __vcmpgtu4(word, 0x20202020u) != 0) ||
+                         pos + 4 + 4 * sz > ch.n_words;
+        if (bad) {
+          werr = -1;  // an earlier unit reports it
+          break;
         }
-        werr = __shfl_sync(0xFFFFFFFFu, werr, 0);
-        pos0 = __shfl_sync(0xFFFFFFFFu, pos0, 0);
+        pos += 4 + 4 * sz;
       }
-      uint32_t pos = pos0;
+      pos0 = pos;
       for (uint32_t mb = b0; werr == IZG_OK && mb < b1; mb += 16)
         pos += bp_meta_words(p, pos, min(16u, nblocks - mb), ch.n_words, lane, &werr);
       pos_end = pos;
-      if (lane == 0) {
-        if (werr != IZG_OK) {
-          st_relaxed(&st[k].off, kOffError);
-          if (werr > 0) {  // first error of the chunk in stream order
-            status[c] = werr;
-            if (consumed) consumed[c] = 0;
-          }
-        } else {
-          st_relaxed(&st[k].off, pos_end + 1);
-        }
+      if (lane == 0 && werr > 0) {  // first error of the chunk in stream order
+        status[c] = werr;
+        if (consumed) consumed[c] = 0;
       }
       if (werr != IZG_OK) continue;
     } else if (nblocks) {
@@ -392,6 +413,56 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
         carry.z = __shfl_sync(0xFFFFFFFFu, carry.z, 0);
         carry.w = __shfl_sync(0xFFFFFFFFu, carry.w, 0);
       }
+    }
+    // ---- 2'. reduce-then-scan (SIMD-BP128 array modes): when the
+    // predecessor's prefix is not out yet, sum this segment's deltas (one
+    // unpack pass, no stores), look back, publish the inclusive prefix
+    // before decoding, and decode once with the true carry — no fix-up
+    // traffic.  Step 1 already made every check this segment's payload
+    // needs, so the aggregate is error-free.
+    bool looked_back = false;
+    uint32_t first_err = 0;
+    if (CODEC == IZG_SIMDBP128 && kArray && !have_prefix && nblocks && IZG_SPLIT_RTS) {
+      uint4 agg = make_uint4(0, 0, 0, 0);
+      AggStage as;
+      uint32_t used = 0;
+      r.begin(p + pos0, ch.n_words - pos0);
+      if (r.phase == 0)
+        bp128_core<DELTA, true>(r, as, ch.n_words - pos0, b1, o, oal, orow, agg, &used, b0);
+      else
+        bp128_core<DELTA, false>(r, as, ch.n_words - pos0, b1, o, oal, orow, agg, &used, b0);
+      r.end();
+      uint4 excl = make_uint4(0, 0, 0, 0);
+      if (lane == 0) {
+        publish<DELTA>(st[k].agg, agg, 1u, 0u);
+        for (int32_t j = (int32_t)k - 1; j >= 0; --j) {
+          uint4 v;
+          uint32_t e = 0;
+          for (uint32_t it = 0;; ++it) {
+            if (try_read<DELTA>(st[j].pre, 2u, &v, &e)) {
+              j = -1;
+              break;
+            }
+            if (try_read<DELTA>(st[j].agg, 1u, &v, &e)) break;
+            if (it >= kSpinLimit) {
+              stalled = true;
+              break;
+            }
+            if (it > 32) __nanosleep(64);
+          }
+          if (stalled) break;
+          excl = u4add(excl, v);
+          if (e) first_err = e;
+        }
+        if (stalled) first_err = IZG_E_SPLIT_STALL;
+        publish<DELTA>(st[k].pre, u4add(excl, agg), 2u, first_err);
+      }
+      carry.x = __shfl_sync(0xFFFFFFFFu, excl.x, 0);
+      carry.y = __shfl_sync(0xFFFFFFFFu, excl.y, 0);
+      carry.z = __shfl_sync(0xFFFFFFFFu, excl.z, 0);
+      carry.w = __shfl_sync(0xFFFFFFFFu, excl.w, 0);
+      first_err = __shfl_sync(0xFFFFFFFFu, first_err, 0);
+      have_prefix = looked_back = true;
     }
     int32_t derr = IZG_OK;
     uint32_t pos = 0;
@@ -444,8 +515,9 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
     // ---- 3. look-back (every mode: the chunk's first error travels with
     // the prefixes; the carry is zero without delta coding) ----------------
     uint4 excl = make_uint4(0, 0, 0, 0);
-    uint32_t first_err = 0;
-    if (lane == 0) {
+    if (looked_back) {
+      if (first_err == 0 && derr != IZG_OK) first_err = (uint32_t)derr;  // (not expected)
+    } else if (lane == 0) {
       if (have_prefix) {
         first_err = pre_err;  // the predecessor's prefix is inside `carry`
       } else {
@@ -475,11 +547,13 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
       publish<DELTA>(st[k].pre, u4add(excl, carry), 2u, own);
       first_err = own;
     }
-    excl.x = __shfl_sync(0xFFFFFFFFu, excl.x, 0);
-    excl.y = __shfl_sync(0xFFFFFFFFu, excl.y, 0);
-    excl.z = __shfl_sync(0xFFFFFFFFu, excl.z, 0);
-    excl.w = __shfl_sync(0xFFFFFFFFu, excl.w, 0);
-    first_err = __shfl_sync(0xFFFFFFFFu, first_err, 0);
+    if (!looked_back) {
+      excl.x = __shfl_sync(0xFFFFFFFFu, excl.x, 0);
+      excl.y = __shfl_sync(0xFFFFFFFFu, excl.y, 0);
+      excl.z = __shfl_sync(0xFFFFFFFFu, excl.z, 0);
+      excl.w = __shfl_sync(0xFFFFFFFFu, excl.w, 0);
+      first_err = __shfl_sync(0xFFFFFFFFu, first_err, 0);
+    }
     // ---- 4. fix-up ---------------------------------------------------------
     if (kArray && !have_prefix && first_err == 0)
       seg_fixup<DELTA>(o, oal, b0, b1, core, last ? ch.n : core, excl, lane);

@@ -164,3 +164,34 @@ def test_split_large_batch_forced():
     r = subprocess.run([sys.executable, "-c", _LARGE.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+_SEGS = r'''
+import sys
+sys.path.insert(0, {root!r})
+import torch
+from tests import test_gpu_split as T
+for name in ["simdbp128", "simdbp128-s4", "simdbp128-dm", "simdbp128-d2"]:
+    T.test_split_arrays(torch, name)
+for name in ["simdbp128-s4", "simdbp128"]:
+    T.test_split_corruption_statuses(torch, name)
+print("ok")
+'''
+
+
+@pytest.mark.parametrize("segs", [1, 2, 4, 8])
+def test_split_segment_sizes(segs):
+    """SIMD-BP128 sizes its segments to the batch (split_seg_blocks): every
+    size, forced with IZG_SPLIT_SEGS, against the one-warp kernel — outputs,
+    words consumed, and statuses under corruption (each unit walks the
+    descriptor chain from the chunk start; an error on an earlier segment is
+    reported by its own unit)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IZG_SPLIT_SEGS=str(segs))
+    r = subprocess.run([sys.executable, "-c", _SEGS.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
