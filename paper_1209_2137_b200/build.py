@@ -20,7 +20,7 @@ LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libintzip_b200.so")
 OBJDIR = os.path.join(LIBDIR, "obj")
 
-SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "decode_split.cu", "intersect.cu", "host.cpp", "host_encode.cpp",
+SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "decode_split.cu", "decode_group.cu", "intersect.cu", "host.cpp", "host_encode.cpp",
            "host_datagen.cpp", "container.cpp"]
 # per-source extra flags: see the comment at the top of decode_scalar.cu
 SOURCE_FLAGS = {"decode_scalar.cu": ["-Xptxas", "-O1"]}

@@ -16,6 +16,7 @@
 
 #include "../../include/intzip_b200.h"
 #include "decode_kernel.cuh"
+#include "group.cuh"
 #include "split.cuh"
 #include "encode.cuh"
 
@@ -85,6 +86,27 @@ using SplitFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*,
                          uint32_t*, SplitArgs, IdxView);
 SplitFn pick_split(int codec, int delta);
 
+// SIMD-BP128 group kernels (KW warps per chunk): decode_group.cu.
+using GroupFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
+                         uint32_t*, uint32_t*, const CUtensorMap, int);
+GroupFn pick_group(int kw, int delta);
+
+// Warps per chunk for a SIMD-BP128 batch that does not take the split
+// kernel: the largest KW in {1, 2, 4, 8} whose n_chunks * KW warps fit the
+// resident warp slots, i.e. enough chunks in flight per SM.  IZG_GROUP=1, 2,
+// 4 or 8 forces it (tuning sweeps).
+uint32_t group_warps(uint32_t n_chunks, uint32_t warp_slots) {
+  static const int force = [] {
+    const char* e = std::getenv("IZG_GROUP");
+    const int v = e ? std::atoi(e) : 0;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : 0;
+  }();
+  if (force) return (uint32_t)force;
+  uint32_t kw = 1;
+  while (kw < 8 && (uint64_t)n_chunks * kw * 2 <= warp_slots) kw *= 2;
+  return kw;
+}
+
 // Small batches decode with the split kernel (split.cuh) when the caller
 // gives a workspace: with few chunks one warp per chunk leaves SMs idle.
 // Crossovers measured with tools/split_sweep.py on B200 (65,536-integer
@@ -122,8 +144,8 @@ struct DeviceInfo {
   bool ok = false;
   int sms = 0;
   // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink,
-  //  + 3 kCodecs: split kernels)][delta]
-  int occ[4 * kCodecs][5] = {};
+  //  + 3 kCodecs: split kernels, 4 kCodecs + 0..2: group kernels KW = 2, 4, 8)][delta]
+  int occ[4 * kCodecs + 3][5] = {};
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -243,6 +265,36 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   const bool split = !probe && split_wanted(codec, n_chunks) && d_ws &&
                      (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
                      ws_bytes >= workspace_bytes(codec, n_chunks);
+  if (codec == IZG_SIMDBP128 && !probe && !split) {
+    // warp slots of the one-warp kernel (same registers and ring as the
+    // group kernels): decide how many warps share a chunk
+    int per_sm1 = 0, sms1 = 0;
+    uint32_t* ctr1 = nullptr;
+    int rc1 = prepare(dev, codec, delta, reinterpret_cast<const void*>(fn), warps * 32, smem,
+                      &per_sm1, &sms1, &ctr1);
+    if (rc1 != IZG_SUCCESS) return rc1;
+    const uint32_t kw = group_warps(n_chunks, (uint32_t)(per_sm1 * sms1 * warps));
+    if (kw > 1) {
+      GroupFn gfn = pick_group((int)kw, delta);
+      const size_t gsmem = GroupLayout::kSmem;
+      const int variant = 4 * kCodecs + (kw == 2 ? 0 : kw == 4 ? 1 : 2);
+      int per_sm = 0, sms = 0;
+      uint32_t* counter = nullptr;
+      rc1 = prepare(dev, variant, delta, reinterpret_cast<const void*>(gfn), warps * 32, gsmem,
+                    &per_sm, &sms, &counter);
+      if (rc1 != IZG_SUCCESS) return rc1;
+      cudaStream_t s = static_cast<cudaStream_t>(stream);
+      if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
+      const uint64_t want = ((uint64_t)n_chunks * kw + warps - 1) / warps;
+      const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
+      CUtensorMap omap;
+      std::memset(&omap, 0, sizeof(omap));
+      const int tma_out = make_out_map(&omap, d_out) ? 1 : 0;
+      gfn<<<grid, warps * 32, gsmem, s>>>(d_words, d_chunks, n_chunks, d_out, d_status,
+                                          d_consumed, counter, omap, tma_out);
+      return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+    }
+  }
   const void* kfn = split ? reinterpret_cast<const void*>(pick_split(codec, delta))
                           : reinterpret_cast<const void*>(fn);
   int rc = prepare(dev, codec + (split ? 3 * kCodecs : idx ? kCodecs : probe ? 2 * kCodecs : 0),

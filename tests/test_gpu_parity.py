@@ -178,3 +178,35 @@ def test_device_checksum_large_batch(cuda, name):
     b.decode()
     b.check()
     assert b.checksum() == host_checksum(flat)
+
+
+_GROUP = r'''
+import sys
+sys.path.insert(0, {root!r})
+import torch
+from oracle.pyoracle import Oracle
+from tests import test_gpu_parity as T
+O = Oracle()
+for name in ["simdbp128", "simdbp128-s4", "simdbp128-d2", "simdbp128-dm"]:
+    T.test_roundtrip_assorted(torch, O, name)
+    T.test_mutation_fuzz_matches_oracle(torch, O, name)
+    T.test_unaligned_placement(torch, name, 2, 3)
+print("ok")
+'''
+
+
+@pytest.mark.parametrize("kw", [1, 2, 4, 8])
+def test_bp128_warps_per_chunk(kw):
+    """SIMD-BP128 without the split kernel runs KW warps per chunk on small
+    batches (csrc/group.cuh, iterations round robin, mailbox carry): every
+    KW, forced with IZG_GROUP (1 = the one-warp kernel), against the oracle
+    — outputs and statuses under mutation fuzz, unaligned placements."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IZG_GROUP=str(kw), IZG_SPLIT="0")
+    r = subprocess.run([sys.executable, "-c", _GROUP.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
