@@ -92,9 +92,8 @@ using GroupFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*,
 GroupFn pick_group(int kw, int delta);
 
 // Warps per chunk for a SIMD-BP128 batch that does not take the split
-// kernel: the largest KW in {1, 2, 4, 8} whose n_chunks * KW warps fit the
-// resident warp slots, i.e. enough chunks in flight per SM.  IZG_GROUP=1, 2,
-// 4 or 8 forces it (tuning sweeps).
+// kernel, by batch size against the resident warp slots.  IZG_GROUP=1, 2, 4
+// or 8 forces it (tuning sweeps).
 uint32_t group_warps(uint32_t n_chunks, uint32_t warp_slots) {
   static const int force = [] {
     const char* e = std::getenv("IZG_GROUP");
@@ -102,9 +101,11 @@ uint32_t group_warps(uint32_t n_chunks, uint32_t warp_slots) {
     return v == 1 || v == 2 || v == 4 || v == 8 ? v : 0;
   }();
   if (force) return (uint32_t)force;
-  uint32_t kw = 1;
-  while (kw < 8 && (uint64_t)n_chunks * kw * 2 <= warp_slots) kw *= 2;
-  return kw;
+  // measured (tools/group_ab.sh, 65,536-integer chunks, 3,552 slots): KW 8
+  // best up to ~200 chunks, KW 4 up to ~900, one warp per chunk from 1,024
+  if ((uint64_t)n_chunks * 16 <= warp_slots) return 8;
+  if ((uint64_t)n_chunks * 4 <= warp_slots) return 4;
+  return 1;
 }
 
 // Small batches decode with the split kernel (split.cuh) when the caller
@@ -265,42 +266,38 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   const bool split = !probe && split_wanted(codec, n_chunks) && d_ws &&
                      (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
                      ws_bytes >= workspace_bytes(codec, n_chunks);
-  if (codec == IZG_SIMDBP128 && !probe && !split) {
-    // warp slots of the one-warp kernel (same registers and ring as the
-    // group kernels): decide how many warps share a chunk
-    int per_sm1 = 0, sms1 = 0;
-    uint32_t* ctr1 = nullptr;
-    int rc1 = prepare(dev, codec, delta, reinterpret_cast<const void*>(fn), warps * 32, smem,
-                      &per_sm1, &sms1, &ctr1);
-    if (rc1 != IZG_SUCCESS) return rc1;
-    const uint32_t kw = group_warps(n_chunks, (uint32_t)(per_sm1 * sms1 * warps));
-    if (kw > 1) {
-      GroupFn gfn = pick_group((int)kw, delta);
-      const size_t gsmem = GroupLayout::kSmem;
-      const int variant = 4 * kCodecs + (kw == 2 ? 0 : kw == 4 ? 1 : 2);
-      int per_sm = 0, sms = 0;
-      uint32_t* counter = nullptr;
-      rc1 = prepare(dev, variant, delta, reinterpret_cast<const void*>(gfn), warps * 32, gsmem,
-                    &per_sm, &sms, &counter);
-      if (rc1 != IZG_SUCCESS) return rc1;
-      cudaStream_t s = static_cast<cudaStream_t>(stream);
-      if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
-      const uint64_t want = ((uint64_t)n_chunks * kw + warps - 1) / warps;
-      const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
-      CUtensorMap omap;
-      std::memset(&omap, 0, sizeof(omap));
-      const int tma_out = make_out_map(&omap, d_out) ? 1 : 0;
-      gfn<<<grid, warps * 32, gsmem, s>>>(d_words, d_chunks, n_chunks, d_out, d_status,
-                                          d_consumed, counter, omap, tma_out);
-      return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
-    }
-  }
   const void* kfn = split ? reinterpret_cast<const void*>(pick_split(codec, delta))
                           : reinterpret_cast<const void*>(fn);
   int rc = prepare(dev, codec + (split ? 3 * kCodecs : idx ? kCodecs : probe ? 2 * kCodecs : 0),
                    delta, kfn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;
+  if (codec == IZG_SIMDBP128 && !probe && !split) {
+    // SIMD-BP128 small batches: KW warps per chunk (group.cuh); the one-warp
+    // kernel's warp slots (same registers and ring) set KW
+    // (warp slots as designed: 3 CTAs of 8 warps per SM at 80 registers)
+    const uint32_t kw = group_warps(n_chunks, (uint32_t)(3 * sms * warps));
+    if (kw > 1) {
+      GroupFn gfn = pick_group((int)kw, delta);
+      const size_t gsmem = GroupLayout::kSmem;
+      const int variant = 4 * kCodecs + (kw == 2 ? 0 : kw == 4 ? 1 : 2);
+      int gper_sm = 0, gsms = 0;
+      uint32_t* gcounter = nullptr;
+      rc = prepare(dev, variant, delta, reinterpret_cast<const void*>(gfn), warps * 32, gsmem,
+                   &gper_sm, &gsms, &gcounter);
+      if (rc != IZG_SUCCESS) return rc;
+      cudaStream_t gs = static_cast<cudaStream_t>(stream);
+      if (cudaMemsetAsync(gcounter, 0, sizeof(uint32_t), gs) != cudaSuccess) return IZG_ERR_CUDA;
+      const uint64_t want = ((uint64_t)n_chunks * kw + warps - 1) / warps;
+      const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)gper_sm * gsms);
+      CUtensorMap omap;
+      std::memset(&omap, 0, sizeof(omap));
+      const int tma_out = make_out_map(&omap, d_out) ? 1 : 0;
+      gfn<<<grid, warps * 32, gsmem, gs>>>(d_words, d_chunks, n_chunks, d_out, d_status,
+                                           d_consumed, gcounter, omap, tma_out);
+      return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+    }
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   IdxView ix{};
   if (idx) {
