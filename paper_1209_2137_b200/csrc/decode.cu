@@ -111,11 +111,12 @@ uint32_t group_warps(uint32_t n_chunks, uint32_t warp_slots) {
 // Small batches decode with the split kernel (split.cuh) when the caller
 // gives a workspace: with few chunks one warp per chunk leaves SMs idle.
 // Crossovers measured with tools/split_sweep.py on B200 (65,536-integer
-// chunks): SIMD-BP128 wins up to ~512 chunks (64: 0.035 vs 0.113 ms; 512:
-// 0.101 vs 0.114; 1,024: 0.145 vs 0.115), SIMD-FastPFOR up to ~1,024 pages
-// (64: 0.154 vs 0.379 ms; 1,024: 0.398 vs 0.504 ms).  IZG_SPLIT=0 / 1 in the
-// environment forces it off / on.
-constexpr uint32_t kSplitMaxChunksBp = 512, kSplitMaxChunksFp = 1024;
+// chunks): SIMD-BP128 split wins up to ~300 chunks against the group kernel
+// (64: 0.035 vs 0.066 ms; 256: 0.067 vs 0.076; 512: 0.101 vs 0.089), and
+// SIMD-FastPFOR up to ~1,024 pages against one warp per page (64: 0.154 vs
+// 0.379 ms; 1,024: 0.398 vs 0.504 ms).  IZG_SPLIT=0 / 1 in the environment
+// forces it off / on.
+constexpr uint32_t kSplitMaxChunksBp = 384, kSplitMaxChunksFp = 1024;
 bool split_wanted(int codec, uint32_t n_chunks) {
   if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return false;
   static const int force = [] {
@@ -328,7 +329,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     // smallest (measured best at every batch size it is selected for)
     sa.seg_blocks = codec == IZG_SIMDBP128
                         ? split_seg_blocks(n_chunks, (uint32_t)(per_sm * sms * warps))
-                        : kSegBlocks;
+                        : kFpSegBlocks;
     static const int force_segs = [] {  // IZG_SPLIT_SEGS=1..16: tuning sweeps
       const char* e = std::getenv("IZG_SPLIT_SEGS");
       const int v = e ? std::atoi(e) : 0;

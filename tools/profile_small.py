@@ -1,5 +1,7 @@
 """Decode a small batch (for ncu launch lists): CHUNKS arrays of 65,536.
-    python tools/profile_small.py <simdbp128-s4|simdfastpfor-s4> <chunks> [reps]"""
+    python tools/profile_small.py <simdbp128-s4|simdfastpfor-s4> <chunks> [reps]
+IZG_NOWS=1: no workspace (izg_decode: SIMD-BP128 small batches take the group
+kernel instead of the split kernel)."""
 import os
 import sys
 
@@ -17,7 +19,7 @@ vals, _ = P.gen_arrays("geometric" if geo else "cluster", count, 65536, 32 if ge
                        seed=1, rate_ppm=100000 if geo else 0)
 enc = P.encode_chunks(codec, vals.reshape(-1), np.arange(count, dtype=np.uint64) * 65536,
                       np.full(count, 65536, np.uint32), allow_wrap=geo)
-b = P.DeviceBatch(codec, enc)
+b = P.DeviceBatch(codec, enc, indexed=os.environ.get("IZG_NOWS") != "1")
 for _ in range(reps):
     b.decode()
 torch.cuda.synchronize()
