@@ -191,6 +191,10 @@ __global__ void __maxnreg__((Layout<IZG_SIMDBP128>::kMaxRegs))
     named_bar_sync(1 + grp, KW * 32);
     const uint32_t c = lds32_volatile(slot);
     if (c >= n_chunks) break;
+    // every warp is past the previous chunk: clear its last tag, so no stale
+    // tag can ever match this round's (the first post of the round is warp
+    // 0's own, after this store)
+    if (wi == 0 && lane == 0) sts32_volatile(mbx + 16, 0xFFFFFFFFu);
     const izg_chunk ch = chunks[c];
     int32_t st = precheck(IZG_SIMDBP128, kArray, ch.n);
     uint32_t pos = 0;
