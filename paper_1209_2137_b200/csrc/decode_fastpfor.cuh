@@ -336,6 +336,9 @@ static __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint
 // first OR; the round count is set by the longest of the four lists.
 // Duplicate positions OR together like the reference.  Returns true when a
 // position >= 128 was met (the caller resolves precedence).
+#ifndef IZG_PATCH_SLOTS
+#define IZG_PATCH_SLOTS 2  // exceptions per lane per round (8 lanes per block)
+#endif
 template <int ST>
 __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const uint8_t* ba,
                                          uint32_t myb, uint32_t myw, uint32_t myc, uint32_t mybp,
@@ -345,11 +348,11 @@ __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const
   mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));
   const uint32_t wmask = low_mask(myw), w4 = 4u * myw;
   bool bad = false;
-  for (uint32_t e0 = s8; e0 < mxc; e0 += 16) {
-    uint32_t pp[2], lo[2], hi[2], sh[2];
-    bool ok[2];
+  for (uint32_t e0 = s8; e0 < mxc; e0 += 8 * IZG_PATCH_SLOTS) {
+    uint32_t pp[IZG_PATCH_SLOTS], lo[IZG_PATCH_SLOTS], hi[IZG_PATCH_SLOTS], sh[IZG_PATCH_SLOTS];
+    bool ok[IZG_PATCH_SLOTS];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < IZG_PATCH_SLOTS; ++j) {
       const uint32_t e = e0 + 8u * j;
       ok[j] = e < myc;
       const uint32_t ee = ok[j] ? e : 0u;
@@ -372,7 +375,7 @@ __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const
       hi[j] = ld_u32(page + (ok[j] ? word + (sh[j] + myw > 32 ? step : 0u) : 0u));
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < IZG_PATCH_SLOTS; ++j) {
       if (ok[j]) {
         const uint32_t high = funnel_r(lo[j], hi[j], sh[j]) & wmask;
         if (pp[j] < 128u)
