@@ -220,7 +220,11 @@ __device__ bool fp_blocks_idx(WarpRing& r, OS& os, const uint32_t* dir_base, con
     const uint32_t myoff = e.y, mybp = e.z, mycur = e.w;
     const uint32_t first = __shfl_sync(0xFFFFFFFFu, myoff, 0);
     const uint32_t after = __shfl_sync(0xFFFFFFFFu, myoff + 4u * myb, 8 * (ng - 1));
+#ifdef IZG_ABL_NOEXC  // developer ablation (wrong output): no patch path
+    const bool tot = false;
+#else
     const bool tot = __any_sync(0xFFFFFFFFu, myc != 0);
+#endif
 
     // Stream window: packed words [first, after) (the stream starts at word 1).
     r.release_below(4u * (first - wbase));
@@ -237,7 +241,9 @@ __device__ bool fp_blocks_idx(WarpRing& r, OS& os, const uint32_t* dir_base, con
       const uint32_t t = os.acquire();
       OutStage::write(t, v, lane);
       __syncwarp();
+#ifndef IZG_ABL_NOPATCH  // developer ablation (wrong output): tile round trip only
       bad |= fp_patch<ST>(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
+#endif
       __syncwarp();
       OutStage::read(t, v, lane);
       scan<DELTA>(v, carry, lane);
