@@ -56,6 +56,9 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+#ifndef IZG_TMA_STORE
+#define IZG_TMA_STORE 1  // full iterations leave through TMA tensor stores (else st.global.v4)
+#endif
 bool make_out_map(CUtensorMap* m, uint32_t* out) {
   static EncodeTiledFn fn = [] {
     void* p = nullptr;
@@ -293,7 +296,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
       const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)gper_sm * gsms);
       CUtensorMap omap;
       std::memset(&omap, 0, sizeof(omap));
-      const int tma_out = make_out_map(&omap, d_out) ? 1 : 0;
+      const int tma_out = IZG_TMA_STORE && make_out_map(&omap, d_out) ? 1 : 0;
       gfn<<<grid, warps * 32, gsmem, gs>>>(d_words, d_chunks, n_chunks, d_out, d_status,
                                            d_consumed, gcounter, omap, tma_out);
       return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
@@ -347,7 +350,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
   CUtensorMap omap;
   std::memset(&omap, 0, sizeof(omap));
-  const int tma_out = !probe && make_out_map(&omap, d_out) ? 1 : 0;
+  const int tma_out = !probe && IZG_TMA_STORE && make_out_map(&omap, d_out) ? 1 : 0;
   fn<<<grid, warps * 32, smem, s>>>(d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
                                     counter, omap, tma_out, ix, probe ? *probe : ProbeArgs{});
   return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;

@@ -323,7 +323,13 @@ __device__ int32_t bp128_core(WarpRing& r, OS& os, uint32_t nw, uint32_t nblocks
         accumulate<DELTA>(v, acc);
         continue;
       }
+#ifndef IZG_ABL_BP_NOSCAN  // developer ablation (wrong output): no prefix sum
       scan<DELTA>(v, carry, lane);
+#endif
+#ifdef IZG_ABL_BP_NOSTORE  // developer ablation (no output): nothing stored
+      if (v[0][0] == 0xFFFFFFFFu && v[3][3] == 0x12345678u) carry.x += 1;
+      continue;
+#endif
       if (orow >= 0 && g0 + 4 <= groups) {
         os.put(v, lane, (uint32_t)(orow + 4 * (mb0 + g0)));
       } else {
