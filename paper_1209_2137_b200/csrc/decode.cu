@@ -263,7 +263,9 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;
   uint32_t* counter = nullptr;
-  const int warps = paged ? Layout<IZG_SIMDFASTPFOR>::kWarps : Layout<IZG_SIMDBP128>::kWarps;
+  const int warps = idx     ? Layout<IZG_SIMDFASTPFOR, true>::kWarps
+                    : paged ? Layout<IZG_SIMDFASTPFOR>::kWarps
+                            : Layout<IZG_SIMDBP128>::kWarps;
   const size_t smem = idx     ? Layout<IZG_SIMDFASTPFOR, true>::kSmem
                       : paged ? Layout<IZG_SIMDFASTPFOR>::kSmem
                               : Layout<IZG_SIMDBP128>::kSmem;

@@ -37,7 +37,10 @@ struct Layout {
   // page codecs (byte array + exceptions) vs binary packing
   static constexpr bool kPaged = CODEC == IZG_SIMDFASTPFOR || CODEC == IZG_FASTPFOR ||
                                  CODEC == IZG_SIMPLEPFOR;
-  static constexpr int kWarps = kPaged ? 6 : 8;
+#ifndef IZG_IDX_WARPS
+#define IZG_IDX_WARPS 6
+#endif
+  static constexpr int kWarps = kPaged ? (IDX ? IZG_IDX_WARPS : 6) : 8;
   // registers per thread: 3 CTAs per SM for the fused kernels; the indexed
   // page decode (no parse or metadata state) fits 4 CTAs of 6 warps
 #ifndef IZG_PAGED_MAXREGS
