@@ -54,9 +54,8 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
   constexpr bool kArray = DELTA != IZG_DELTA_NONE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRing r;
-  r.gen = smem + warp * kRingBytes;
-  r.base = smem_u32(r.gen);
-  r.full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff) + warp * kNS;
+  r.base = smem_u32(smem + warp * kRingBytes);
+  r.bar = smem_u32(smem + LY::kBarOff) + warp * kNS * 8u;
   FpScratch* fsc = reinterpret_cast<FpScratch*>(smem + LY::kTabOff + warp * LY::kTabBytes);
   OS os;
   os.base = smem_u32(smem + LY::kOutOff + warp * 2 * kStageOut);
@@ -71,7 +70,7 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
   r.leader = lane == 0;
   r.policy = policy_evict_first();
   if (lane == 0) {
-    for (uint32_t i = 0; i < kNS; ++i) mbar_init(&r.full[i], 1);
+    for (uint32_t i = 0; i < kNS; ++i) mbar_init_s(r.bar + 8u * i, 1);
     fence_barrier_init();
   }
   __syncwarp();

@@ -167,9 +167,8 @@ __global__ void __maxnreg__((Layout<IZG_SIMDBP128>::kMaxRegs))
   const uint32_t grp = (uint32_t)warp / KW, wi = (uint32_t)warp % KW;
   const uint32_t mbx = smem_u32(smem + GroupLayout::kMbxOff + 64 * grp);
   WarpRing r;
-  r.gen = smem + warp * kRingBytes;
-  r.base = smem_u32(r.gen);
-  r.full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff) + warp * kNS;
+  r.base = smem_u32(smem + warp * kRingBytes);
+  r.bar = smem_u32(smem + LY::kBarOff) + warp * kNS * 8u;
   OutStage os;
   os.base = smem_u32(smem + LY::kOutOff + warp * 2 * kStageOut);
   os.leader = lane == 0;
@@ -179,7 +178,7 @@ __global__ void __maxnreg__((Layout<IZG_SIMDBP128>::kMaxRegs))
   r.leader = lane == 0;
   r.policy = policy_evict_first();
   if (lane == 0) {
-    for (uint32_t i = 0; i < kNS; ++i) mbar_init(&r.full[i], 1);
+    for (uint32_t i = 0; i < kNS; ++i) mbar_init_s(r.bar + 8u * i, 1);
     fence_barrier_init();
     if (wi == 0) sts32_volatile(mbx + 16, 0xFFFFFFFFu);
   }

@@ -151,16 +151,15 @@ __global__ void __launch_bounds__(kIdxWarps * 32)
     return;
   }
   WarpRing r;
-  r.gen = smem + warp * kRingBytes;
-  r.base = smem_u32(r.gen);
-  r.full = reinterpret_cast<uint64_t*>(smem + IdxLayout::kBarOff) + warp * kNS;
+  r.base = smem_u32(smem + warp * kRingBytes);
+  r.bar = smem_u32(smem + IdxLayout::kBarOff) + warp * kNS * 8u;
   r.g = 0;
   r.leader = lane == 0;
   r.policy = policy_evict_last();  // the decode kernel re-reads the position bytes
   FpScratch& sc = *reinterpret_cast<FpScratch*>(smem + IdxLayout::kScOff + warp * IdxLayout::kScBytes);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + IdxLayout::kCntOff) + warp * 36;
   if (lane == 0) {
-    for (uint32_t i = 0; i < kNS; ++i) mbar_init(&r.full[i], 1);
+    for (uint32_t i = 0; i < kNS; ++i) mbar_init_s(r.bar + 8u * i, 1);
     fence_barrier_init();
   }
   __syncwarp();

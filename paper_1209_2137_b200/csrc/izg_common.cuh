@@ -64,8 +64,7 @@ struct Layout {
 // covering them; `phase` is payload word 0's byte offset in that span.
 struct WarpRing {
   uint32_t base;        // shared address of the ring
-  uint8_t* gen;         // generic pointer to the ring (bulk-copy target)
-  uint64_t* full;       // kNS mbarriers
+  uint32_t bar;         // shared address of its kNS mbarriers (8 bytes each)
   uint32_t g;           // stages consumed before the current chunk
   const uint8_t* a16;   // current chunk span
   uint32_t total, phase, nst;
@@ -86,8 +85,8 @@ struct WarpRing {
         const uint32_t slot = (g + issued) % kNS;
         const uint32_t off = issued * kSB;
         const uint32_t bytes = min(kSB, total - off);
-        mbar_arrive_expect_tx(&full[slot], bytes);
-        bulk_g2s(gen + slot * kSB, a16 + off, bytes, &full[slot], policy);
+        mbar_arrive_expect_tx_s(bar + 8u * slot, bytes);
+        bulk_g2s_s(base + slot * kSB, a16 + off, bytes, bar + 8u * slot, policy);
       }
       ++issued;
     }
@@ -110,7 +109,7 @@ struct WarpRing {
     const uint32_t need = phase + end;
     while (waited * kSB < need && waited < issued) {
       const uint32_t gg = g + waited;
-      mbar_wait(&full[gg % kNS], (gg / kNS) & 1u);
+      mbar_wait_s(bar + 8u * (gg % kNS), (gg / kNS) & 1u);
       ++waited;
     }
   }

@@ -293,9 +293,8 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRing r;
-  r.gen = smem + warp * kRingBytes;
-  r.base = smem_u32(r.gen);
-  r.full = reinterpret_cast<uint64_t*>(smem + LY::kBarOff) + warp * kNS;
+  r.base = smem_u32(smem + warp * kRingBytes);
+  r.bar = smem_u32(smem + LY::kBarOff) + warp * kNS * 8u;
   r.g = 0;
   r.leader = lane == 0;
   r.policy = policy_evict_first();
@@ -303,7 +302,7 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
   SegStage os;
   os.base = smem_u32(smem + LY::kOutOff + warp * 2 * kStageOut);
   if (lane == 0) {
-    for (uint32_t i = 0; i < kNS; ++i) mbar_init(&r.full[i], 1);
+    for (uint32_t i = 0; i < kNS; ++i) mbar_init_s(r.bar + 8u * i, 1);
     fence_barrier_init();
   }
   __syncwarp();
