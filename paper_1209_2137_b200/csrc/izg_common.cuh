@@ -38,16 +38,17 @@ struct Layout {
   static constexpr bool kPaged = CODEC == IZG_SIMDFASTPFOR || CODEC == IZG_FASTPFOR ||
                                  CODEC == IZG_SIMPLEPFOR;
 #ifndef IZG_IDX_WARPS
-#define IZG_IDX_WARPS 6
+#define IZG_IDX_WARPS 4  // with 96 registers: 5 CTAs, 20 warps per SM
 #endif
   static constexpr int kWarps = kPaged ? (IDX ? IZG_IDX_WARPS : 6) : 8;
   // registers per thread: 3 CTAs per SM for the fused kernels; the indexed
-  // page decode (no parse or metadata state) fits 4 CTAs of 6 warps
+  // page decode runs 5 CTAs of 4 warps at 96 registers (no spills; measured
+  // better than 24 warps at 80 registers)
 #ifndef IZG_PAGED_MAXREGS
 #define IZG_PAGED_MAXREGS 96
 #endif
 #ifndef IZG_IDX_MAXREGS
-#define IZG_IDX_MAXREGS 80
+#define IZG_IDX_MAXREGS 96
 #endif
   static constexpr int kMaxRegs = !kPaged ? 80 : IDX ? IZG_IDX_MAXREGS : IZG_PAGED_MAXREGS;
   // per-warp scratch, 16-byte multiple: the fused page kernels' FpScratch
