@@ -40,7 +40,10 @@ struct Layout {
 #ifndef IZG_IDX_WARPS
 #define IZG_IDX_WARPS 4  // with 96 registers: 5 CTAs, 20 warps per SM
 #endif
-  static constexpr int kWarps = kPaged ? (IDX ? IZG_IDX_WARPS : 6) : 8;
+#ifndef IZG_PAGED_WARPS
+#define IZG_PAGED_WARPS 4  // fused page kernels: 5 CTAs of 4 warps at 96 registers
+#endif
+  static constexpr int kWarps = kPaged ? (IDX ? IZG_IDX_WARPS : IZG_PAGED_WARPS) : 8;
   // registers per thread: 3 CTAs per SM for the fused kernels; the indexed
   // page decode runs 5 CTAs of 4 warps at 96 registers (no spills; measured
   // better than 24 warps at 80 registers)

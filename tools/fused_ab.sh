@@ -1,0 +1,4 @@
+for v in default pw4 pw4r80 default; do
+  if [ $v = default ]; then unset IZG_LIB_PATH; else export IZG_LIB_PATH=$PWD/paper_1209_2137_b200/_lib/variants/$v.so; fi
+  echo "== $v"; IZG_FUSED=1 timeout 300 python tools/quick_bench.py c5fp c4 | cut -c1-200; timeout 300 python tools/f3_bench.py 2>&1 | grep -E "fastpfor-s4|simplepfor" | cut -c1-160
+done
