@@ -106,8 +106,9 @@ uint32_t group_warps(uint32_t n_chunks, uint32_t warp_slots) {
   if (force) return (uint32_t)force;
   // measured (tools/group_ab.sh, 65,536-integer chunks, 3,552 slots): KW 8
   // best up to ~200 chunks, KW 4 up to ~900, one warp per chunk from 1,024
-  if ((uint64_t)n_chunks * 16 <= warp_slots) return 8;
-  if ((uint64_t)n_chunks * 4 <= warp_slots) return 4;
+  constexpr uint32_t kMaxKw = Layout<IZG_SIMDBP128>::kWarps;  // a group lives in one CTA
+  if ((uint64_t)n_chunks * 16 <= warp_slots) return kMaxKw >= 8 ? 8 : kMaxKw;
+  if ((uint64_t)n_chunks * 4 <= warp_slots) return kMaxKw >= 4 ? 4 : kMaxKw;
   return 1;
 }
 
@@ -282,7 +283,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     // SIMD-BP128 small batches: KW warps per chunk (group.cuh); the one-warp
     // kernel's warp slots (same registers and ring) set KW
     // (warp slots as designed: 3 CTAs of 8 warps per SM at 80 registers)
-    const uint32_t kw = group_warps(n_chunks, (uint32_t)(3 * sms * warps));
+    const uint32_t kw = group_warps(n_chunks, (uint32_t)(24 * sms));
     if (kw > 1) {
       GroupFn gfn = pick_group((int)kw, delta);
       const size_t gsmem = GroupLayout::kSmem;

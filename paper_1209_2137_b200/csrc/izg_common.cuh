@@ -43,7 +43,13 @@ struct Layout {
 #ifndef IZG_PAGED_WARPS
 #define IZG_PAGED_WARPS 4  // fused page kernels: 5 CTAs of 4 warps at 96 registers
 #endif
-  static constexpr int kWarps = kPaged ? (IDX ? IZG_IDX_WARPS : IZG_PAGED_WARPS) : 8;
+#ifndef IZG_BP_WARPS
+#define IZG_BP_WARPS 8
+#endif
+#ifndef IZG_BP_MAXREGS
+#define IZG_BP_MAXREGS 80
+#endif
+  static constexpr int kWarps = kPaged ? (IDX ? IZG_IDX_WARPS : IZG_PAGED_WARPS) : IZG_BP_WARPS;
   // registers per thread: 3 CTAs per SM for the fused kernels; the indexed
   // page decode runs 5 CTAs of 4 warps at 96 registers (no spills; measured
   // better than 24 warps at 80 registers)
@@ -53,7 +59,7 @@ struct Layout {
 #ifndef IZG_IDX_MAXREGS
 #define IZG_IDX_MAXREGS 96
 #endif
-  static constexpr int kMaxRegs = !kPaged ? 80 : IDX ? IZG_IDX_MAXREGS : IZG_PAGED_MAXREGS;
+  static constexpr int kMaxRegs = !kPaged ? IZG_BP_MAXREGS : IDX ? IZG_IDX_MAXREGS : IZG_PAGED_MAXREGS;
   // per-warp scratch, 16-byte multiple: the fused page kernels' FpScratch
   // (decode_fastpfor.cuh), the indexed one's exception directory only
   static constexpr uint32_t kTabBytes = !kPaged ? 0 : IDX ? 144 : 2048 + 512 + 2 * 33 * 4 + 8;
