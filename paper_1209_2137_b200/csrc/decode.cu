@@ -121,6 +121,14 @@ uint32_t group_warps(uint32_t n_chunks, uint32_t warp_slots) {
 // 0.379 ms; 1,024: 0.398 vs 0.504 ms).  IZG_SPLIT=0 / 1 in the environment
 // forces it off / on.
 constexpr uint32_t kSplitMaxChunksBp = 384, kSplitMaxChunksFp = 1024;
+// Indexed SIMD-FastPFOR batches from this many pages on use the 24-warp,
+// 80-register decode shape (C5's 65,536 pages: 7.00 vs 7.09 ms); below it
+// the 20-warp, 96-register one (8,192 C5 pages: 1.038 vs 1.053 ms; C4's
+// 2,048: 0.571 vs 0.617).
+#ifndef IZG_BIG_IDX_BATCH
+#define IZG_BIG_IDX_BATCH 24576
+#endif
+constexpr uint32_t kBigIdxBatch = IZG_BIG_IDX_BATCH;
 bool split_wanted(int codec, uint32_t n_chunks) {
   if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return false;
   static const int force = [] {
@@ -151,7 +159,7 @@ struct DeviceInfo {
   int sms = 0;
   // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink,
   //  + 3 kCodecs: split kernels, 4 kCodecs + 0..2: group kernels KW = 2, 4, 8)][delta]
-  int occ[4 * kCodecs + 3][5] = {};
+  int occ[4 * kCodecs + 4][5] = {};
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -250,12 +258,20 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   const bool idx = !probe && codec == IZG_SIMDFASTPFOR && d_ws &&
                    (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
                    ws_bytes >= idx_workspace_bytes(n_chunks);
+  // very large indexed batches: the 24-warp shape (Layout SHAPE 1)
+  static const uint32_t big_from = [] {  // IZG_BIG_IDX_BATCH=n: tests / tuning
+    const char* e = std::getenv("IZG_BIG_IDX_BATCH");
+    return e ? (uint32_t)std::strtoul(e, nullptr, 10) : kBigIdxBatch;
+  }();
+  const bool big = idx && n_chunks >= big_from;
   KernelFn fn = nullptr;
   switch (codec) {
     case IZG_SIMDBP128: fn = pick<IZG_SIMDBP128, false>(delta); break;
     case IZG_BP32: fn = pick<IZG_BP32, false>(delta); break;
     case IZG_SIMDFASTPFOR:
-      fn = idx ? pick<IZG_SIMDFASTPFOR, true>(delta) : pick<IZG_SIMDFASTPFOR, false>(delta);
+      fn = big ? pick<IZG_SIMDFASTPFOR, true, 1>(delta)
+           : idx ? pick<IZG_SIMDFASTPFOR, true>(delta)
+                 : pick<IZG_SIMDFASTPFOR, false>(delta);
       break;
     case IZG_FASTPFOR: fn = pick_fastpfor_scalar(delta); break;
     case IZG_SIMPLEPFOR: fn = pick<IZG_SIMPLEPFOR, false>(delta); break;
@@ -264,10 +280,12 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   DeviceGuard guard(dev);
   int per_sm = 0, sms = 0;
   uint32_t* counter = nullptr;
-  const int warps = idx     ? Layout<IZG_SIMDFASTPFOR, true>::kWarps
+  const int warps = big     ? Layout<IZG_SIMDFASTPFOR, true, 1>::kWarps
+                    : idx   ? Layout<IZG_SIMDFASTPFOR, true>::kWarps
                     : paged ? Layout<IZG_SIMDFASTPFOR>::kWarps
                             : Layout<IZG_SIMDBP128>::kWarps;
-  const size_t smem = idx     ? Layout<IZG_SIMDFASTPFOR, true>::kSmem
+  const size_t smem = big     ? Layout<IZG_SIMDFASTPFOR, true, 1>::kSmem
+                      : idx   ? Layout<IZG_SIMDFASTPFOR, true>::kSmem
                       : paged ? Layout<IZG_SIMDFASTPFOR>::kSmem
                               : Layout<IZG_SIMDBP128>::kSmem;
   const bool split = !probe && split_wanted(codec, n_chunks) && d_ws &&
@@ -275,7 +293,8 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                      ws_bytes >= workspace_bytes(codec, n_chunks);
   const void* kfn = split ? reinterpret_cast<const void*>(pick_split(codec, delta))
                           : reinterpret_cast<const void*>(fn);
-  int rc = prepare(dev, codec + (split ? 3 * kCodecs : idx ? kCodecs : probe ? 2 * kCodecs : 0),
+  int rc = prepare(dev, big ? 4 * kCodecs + 3
+                           : codec + (split ? 3 * kCodecs : idx ? kCodecs : probe ? 2 * kCodecs : 0),
                    delta, kfn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;

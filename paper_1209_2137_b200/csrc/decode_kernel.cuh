@@ -41,16 +41,16 @@ __device__ __forceinline__ int32_t precheck(int codec, bool array_mode, uint32_t
 // pages were indexed by fp_index_kernel into `ix`.  OS is the output sink:
 // OutStage writes the decoded integers to `out`; ProbeStage (probe.cuh)
 // intersects them with `pa.s` instead and `out` is unused.
-template <int CODEC, int DELTA, bool IDX, typename OS = OutStage>
-__global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
-    __maxnreg__((Layout<CODEC, IDX>::kMaxRegs))
+template <int CODEC, int DELTA, bool IDX, typename OS = OutStage, int SHAPE = 0>
+__global__ void __launch_bounds__((Layout<CODEC, IDX, SHAPE>::kWarps * 32))
+    __maxnreg__((Layout<CODEC, IDX, SHAPE>::kMaxRegs))
     decode_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                   uint32_t n_chunks, uint32_t* __restrict__ out, int32_t* __restrict__ status,
                   uint32_t* __restrict__ consumed, uint32_t* __restrict__ next_chunk,
                   const __grid_constant__ CUtensorMap omap, int tma_out, IdxView ix,
                   ProbeArgs pa) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  using LY = Layout<CODEC, IDX>;
+  using LY = Layout<CODEC, IDX, SHAPE>;
   constexpr bool kArray = DELTA != IZG_DELTA_NONE;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpRing r;
@@ -164,14 +164,14 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX>::kWarps * 32))
 using KernelFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
                           uint32_t*, uint32_t*, const CUtensorMap, int, IdxView, ProbeArgs);
 
-template <int CODEC, bool IDX>
+template <int CODEC, bool IDX, int SHAPE = 0>
 KernelFn pick(int delta) {
   switch (delta) {
-    case IZG_DELTA_NONE: return decode_kernel<CODEC, IZG_DELTA_NONE, IDX>;
-    case IZG_DELTA_D1: return decode_kernel<CODEC, IZG_DELTA_D1, IDX>;
-    case IZG_DELTA_D4: return decode_kernel<CODEC, IZG_DELTA_D4, IDX>;
-    case IZG_DELTA_D2: return decode_kernel<CODEC, IZG_DELTA_D2, IDX>;
-    case IZG_DELTA_DM: return decode_kernel<CODEC, IZG_DELTA_DM, IDX>;
+    case IZG_DELTA_NONE: return decode_kernel<CODEC, IZG_DELTA_NONE, IDX, OutStage, SHAPE>;
+    case IZG_DELTA_D1: return decode_kernel<CODEC, IZG_DELTA_D1, IDX, OutStage, SHAPE>;
+    case IZG_DELTA_D4: return decode_kernel<CODEC, IZG_DELTA_D4, IDX, OutStage, SHAPE>;
+    case IZG_DELTA_D2: return decode_kernel<CODEC, IZG_DELTA_D2, IDX, OutStage, SHAPE>;
+    case IZG_DELTA_DM: return decode_kernel<CODEC, IZG_DELTA_DM, IDX, OutStage, SHAPE>;
   }
   return nullptr;
 }

@@ -32,7 +32,10 @@ constexpr uint32_t kStageOut = 2048;          // one warp iteration of output (5
 // Shared memory per CTA: the warps' rings, then 2 output staging tiles per
 // warp (1024-byte aligned for the 128-byte TMA swizzle), then per-warp
 // SIMD-FastPFOR block tables, then the ring barriers.
-template <int CODEC, bool IDX = false>
+// SHAPE (indexed SIMD-FastPFOR only): 0 = 4 warps per CTA at 96 registers
+// (20 warps per SM), 1 = 6 warps at 80 registers (24 per SM) for very large
+// batches, whose page records come from HBM rather than L2.
+template <int CODEC, bool IDX = false, int SHAPE = 0>
 struct Layout {
   // page codecs (byte array + exceptions) vs binary packing
   static constexpr bool kPaged = CODEC == IZG_SIMDFASTPFOR || CODEC == IZG_FASTPFOR ||
@@ -49,7 +52,8 @@ struct Layout {
 #ifndef IZG_BP_MAXREGS
 #define IZG_BP_MAXREGS 80
 #endif
-  static constexpr int kWarps = kPaged ? (IDX ? IZG_IDX_WARPS : IZG_PAGED_WARPS) : IZG_BP_WARPS;
+  static constexpr int kWarps =
+      kPaged ? (IDX ? (SHAPE ? 6 : IZG_IDX_WARPS) : IZG_PAGED_WARPS) : IZG_BP_WARPS;
   // registers per thread: 3 CTAs per SM for the fused kernels; the indexed
   // page decode runs 5 CTAs of 4 warps at 96 registers (no spills; measured
   // better than 24 warps at 80 registers)
@@ -59,7 +63,9 @@ struct Layout {
 #ifndef IZG_IDX_MAXREGS
 #define IZG_IDX_MAXREGS 96
 #endif
-  static constexpr int kMaxRegs = !kPaged ? IZG_BP_MAXREGS : IDX ? IZG_IDX_MAXREGS : IZG_PAGED_MAXREGS;
+  static constexpr int kMaxRegs = !kPaged ? IZG_BP_MAXREGS
+                                 : IDX    ? (SHAPE ? 80 : IZG_IDX_MAXREGS)
+                                          : IZG_PAGED_MAXREGS;
   // per-warp scratch, 16-byte multiple: the fused page kernels' FpScratch
   // (decode_fastpfor.cuh), the indexed one's exception directory only
   static constexpr uint32_t kTabBytes = !kPaged ? 0 : IDX ? 144 : 2048 + 512 + 2 * 33 * 4 + 8;

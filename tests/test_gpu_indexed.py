@@ -215,3 +215,34 @@ def test_workspace_too_small_falls_back_to_fused(cuda):
     assert N.lib().izg_decode_workspace_size(0, n) == 0
     assert N.lib().izg_decode_workspace_size(1, n) == n * (16 + 128 + 512 * 16)
     assert N.lib().izg_decode_workspace_size(1, 100) > 100 * (16 + 128 + 512 * 16)
+
+
+_BIG = r'''
+import sys
+sys.path.insert(0, {root!r})
+import torch
+from oracle.pyoracle import Oracle
+from tests import test_gpu_indexed as T
+O = Oracle()
+for name in T.FP_NAMES:
+    T.test_structural_mutations_array(torch, O, name)
+    T.test_random_byte_fuzz_both_paths(torch, name)
+for name in ["simdfastpfor", "simdfastpfor-s4"]:
+    T.test_structural_mutations_raw(torch, O, name)
+print("ok")
+'''
+
+
+def test_large_batch_shape():
+    """The indexed decode's large-batch shape (24 warps at 80 registers, taken
+    from IZG_BIG_IDX_BATCH pages on) forced onto the small batches of this
+    file: statuses and outputs against the oracle and the fused path."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IZG_BIG_IDX_BATCH="1", IZG_SPLIT="0")
+    r = subprocess.run([sys.executable, "-c", _BIG.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
