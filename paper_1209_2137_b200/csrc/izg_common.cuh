@@ -46,6 +46,9 @@ struct Layout {
 #ifndef IZG_PAGED_WARPS
 #define IZG_PAGED_WARPS 4  // fused page kernels: 5 CTAs of 4 warps at 96 registers
 #endif
+#ifndef IZG_BIG_WARPS
+#define IZG_BIG_WARPS 6  // indexed SIMD-FastPFOR, SHAPE 1 (80 registers)
+#endif
 #ifndef IZG_BP_WARPS
 #define IZG_BP_WARPS 8
 #endif
@@ -53,7 +56,7 @@ struct Layout {
 #define IZG_BP_MAXREGS 80
 #endif
   static constexpr int kWarps =
-      kPaged ? (IDX ? (SHAPE ? 6 : IZG_IDX_WARPS) : IZG_PAGED_WARPS) : IZG_BP_WARPS;
+      kPaged ? (IDX ? (SHAPE ? IZG_BIG_WARPS : IZG_IDX_WARPS) : IZG_PAGED_WARPS) : IZG_BP_WARPS;
   // registers per thread: 3 CTAs per SM for the fused kernels; the indexed
   // page decode runs 5 CTAs of 4 warps at 96 registers (no spills; measured
   // better than 24 warps at 80 registers)
