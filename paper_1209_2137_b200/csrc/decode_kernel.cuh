@@ -58,7 +58,7 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX, SHAPE>::kWarps * 32))
   r.bar = smem_u32(smem + LY::kBarOff) + warp * kNS * 8u;
   FpScratch* fsc = reinterpret_cast<FpScratch*>(smem + LY::kTabOff + warp * LY::kTabBytes);
   OS os;
-  os.base = smem_u32(smem + LY::kOutOff + warp * 2 * kStageOut);
+  os.base = smem_u32(smem + LY::kOutOff + warp * LY::kTiles * kStageOut);
   os.leader = lane == 0;
   if constexpr (OS::kProbe) {
     os.pa = pa;
@@ -126,8 +126,8 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX, SHAPE>::kWarps * 32))
           // (vbyte_tail writes out[core + i], hence the offset base)
           uint32_t* tail = nullptr;
           if constexpr (OS::kProbe)
-            tail = reinterpret_cast<uint32_t*>(smem + LY::kOutOff + warp * 2 * kStageOut +
-                                               kStageOut);
+            tail = reinterpret_cast<uint32_t*>(smem + LY::kOutOff +
+                                               warp * LY::kTiles * kStageOut + kStageOut);
           if (lane == 0)
             st = vbyte_tail<DELTA>(reinterpret_cast<const uint8_t*>(p + pos),
                                    4u * (ch.n_words - pos), core, cnt, carry,
@@ -166,12 +166,13 @@ using KernelFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*
 
 template <int CODEC, bool IDX, int SHAPE = 0>
 KernelFn pick(int delta) {
+  using OS = OutStageT<Layout<CODEC, IDX, SHAPE>::kTiles>;
   switch (delta) {
-    case IZG_DELTA_NONE: return decode_kernel<CODEC, IZG_DELTA_NONE, IDX, OutStage, SHAPE>;
-    case IZG_DELTA_D1: return decode_kernel<CODEC, IZG_DELTA_D1, IDX, OutStage, SHAPE>;
-    case IZG_DELTA_D4: return decode_kernel<CODEC, IZG_DELTA_D4, IDX, OutStage, SHAPE>;
-    case IZG_DELTA_D2: return decode_kernel<CODEC, IZG_DELTA_D2, IDX, OutStage, SHAPE>;
-    case IZG_DELTA_DM: return decode_kernel<CODEC, IZG_DELTA_DM, IDX, OutStage, SHAPE>;
+    case IZG_DELTA_NONE: return decode_kernel<CODEC, IZG_DELTA_NONE, IDX, OS, SHAPE>;
+    case IZG_DELTA_D1: return decode_kernel<CODEC, IZG_DELTA_D1, IDX, OS, SHAPE>;
+    case IZG_DELTA_D4: return decode_kernel<CODEC, IZG_DELTA_D4, IDX, OS, SHAPE>;
+    case IZG_DELTA_D2: return decode_kernel<CODEC, IZG_DELTA_D2, IDX, OS, SHAPE>;
+    case IZG_DELTA_DM: return decode_kernel<CODEC, IZG_DELTA_DM, IDX, OS, SHAPE>;
   }
   return nullptr;
 }

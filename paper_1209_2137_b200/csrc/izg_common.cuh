@@ -46,6 +46,15 @@ struct Layout {
 #ifndef IZG_PAGED_WARPS
 #define IZG_PAGED_WARPS 4  // fused page kernels: 5 CTAs of 4 warps at 96 registers
 #endif
+#ifndef IZG_BIG_TILES
+#define IZG_BIG_TILES 1
+#endif
+#ifndef IZG_IDX_TILES
+#define IZG_IDX_TILES 1
+#endif
+#ifndef IZG_PAGED_TILES
+#define IZG_PAGED_TILES 2
+#endif
 #ifndef IZG_BIG_WARPS
 #define IZG_BIG_WARPS 6  // indexed SIMD-FastPFOR, SHAPE 1 (80 registers)
 #endif
@@ -72,8 +81,13 @@ struct Layout {
   // per-warp scratch, 16-byte multiple: the fused page kernels' FpScratch
   // (decode_fastpfor.cuh), the indexed one's exception directory only
   static constexpr uint32_t kTabBytes = !kPaged ? 0 : IDX ? 144 : 2048 + 512 + 2 * 33 * 4 + 8;
+  // output tiles per warp: 2, or 1 for the large-batch indexed shape
+  // (IZG_BIG_TILES) — less shared memory, more L1 for the exception loads
+  static constexpr int kTiles = !kPaged ? 2
+                                : IDX   ? (SHAPE ? IZG_BIG_TILES : IZG_IDX_TILES)
+                                        : IZG_PAGED_TILES;
   static constexpr uint32_t kOutOff = kWarps * kRingBytes;
-  static constexpr uint32_t kTabOff = kOutOff + kWarps * 2 * kStageOut;
+  static constexpr uint32_t kTabOff = kOutOff + kWarps * kTiles * kStageOut;
   static constexpr uint32_t kBarOff = kTabOff + kWarps * kTabBytes;
   static constexpr size_t kSmem = kBarOff + kWarps * kNS * 8;
 };
@@ -284,7 +298,8 @@ __device__ __forceinline__ void store_direct(const uint32_t (&v)[4][4], uint32_t
 // for mapping C: the 8 lanes of a quarter-warp land in 8 distinct 16-byte
 // bank groups), then one TMA tensor store writes 16 full 128-byte rows.
 // Two tiles per warp alternate; a tile is reused once its store has read it.
-struct OutStage {
+template <int NT = 2>  // output tiles per warp (1: the store must have read it first)
+struct OutStageT {
   static constexpr bool kProbe = false;  // see ProbeStage (probe.cuh)
   static constexpr bool kAgg = false;    // see AggStage (split.cuh)
   uint32_t base;     // shared address of the warp's two tiles (1024-aligned)
@@ -300,7 +315,7 @@ struct OutStage {
   }
 
   __device__ __forceinline__ void put(const uint32_t (&v)[4][4], int lane, uint32_t row) {
-    if (leader) bulk_wait_read<1>();
+    if (leader) bulk_wait_read<NT - 1>();
     __syncwarp();
     const uint32_t t = base + buf * kStageOut;
     const uint32_t q = lane >> 3, s8 = lane & 7;
@@ -316,12 +331,12 @@ struct OutStage {
       tma_store_2d(tmap, t, 0, (int)row);
       bulk_commit();
     }
-    buf ^= 1u;
+    buf = NT == 2 ? buf ^ 1u : 0u;
   }
   // Split form for SIMD-FastPFOR, which patches the tile in place:
   // acquire() -> write/patch/read the tile -> commit() or abandon().
   __device__ __forceinline__ uint32_t acquire() {
-    if (leader) bulk_wait_read<1>();
+    if (leader) bulk_wait_read<NT - 1>();
     __syncwarp();
     return base + buf * kStageOut;
   }
@@ -334,7 +349,7 @@ struct OutStage {
       tma_store_2d(tmap, t, 0, (int)row);
       bulk_commit();
     }
-    buf ^= 1u;
+    buf = NT == 2 ? buf ^ 1u : 0u;
   }
   __device__ __forceinline__ void abandon() { __syncwarp(); }
 
@@ -360,6 +375,7 @@ struct OutStage {
     __syncwarp();
   }
 };
+using OutStage = OutStageT<2>;
 
 // Variable Byte remainder (codec_basic.cpp:27-51) of a chunk (at most 127
 // integers), decoded by one lane straight from global memory and continued

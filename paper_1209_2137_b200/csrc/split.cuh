@@ -300,7 +300,7 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
   r.policy = policy_evict_first();
   uint32_t* dir_base = reinterpret_cast<uint32_t*>(smem + LY::kTabOff + warp * LY::kTabBytes);
   SegStage os;
-  os.base = smem_u32(smem + LY::kOutOff + warp * 2 * kStageOut);
+  os.base = smem_u32(smem + LY::kOutOff + warp * LY::kTiles * kStageOut);
   if (lane == 0) {
     for (uint32_t i = 0; i < kNS; ++i) mbar_init_s(r.bar + 8u * i, 1);
     fence_barrier_init();
