@@ -121,13 +121,13 @@ __global__ void __launch_bounds__((Layout<CODEC, IDX, SHAPE>::kWarps * 32))
           // Variable Byte remainder (codec.cpp:56-62).
           uint32_t rb = 0;
           const uint32_t cnt = ch.n - core;
-          // probe sink: the tail goes to the warp's second (idle) tile,
+          // probe sink: the tail goes to the warp's (now idle) tile,
           // linear, then through the probe like any short iteration
           // (vbyte_tail writes out[core + i], hence the offset base)
           uint32_t* tail = nullptr;
           if constexpr (OS::kProbe)
             tail = reinterpret_cast<uint32_t*>(smem + LY::kOutOff +
-                                               warp * LY::kTiles * kStageOut + kStageOut);
+                                               warp * LY::kTiles * kStageOut);
           if (lane == 0)
             st = vbyte_tail<DELTA>(reinterpret_cast<const uint8_t*>(p + pos),
                                    4u * (ch.n_words - pos), core, cnt, carry,

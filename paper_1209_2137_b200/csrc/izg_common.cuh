@@ -53,7 +53,7 @@ struct Layout {
 #define IZG_IDX_TILES 1
 #endif
 #ifndef IZG_PAGED_TILES
-#define IZG_PAGED_TILES 2
+#define IZG_PAGED_TILES 1
 #endif
 #ifndef IZG_BIG_WARPS
 #define IZG_BIG_WARPS 6  // indexed SIMD-FastPFOR, SHAPE 1 (80 registers)
