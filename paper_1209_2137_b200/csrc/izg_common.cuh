@@ -297,8 +297,11 @@ __device__ __forceinline__ void store_direct(const uint32_t (&v)[4][4], uint32_t
 // go to a 2 KiB shared tile in the 128-byte-swizzled layout (conflict-free
 // for mapping C: the 8 lanes of a quarter-warp land in 8 distinct 16-byte
 // bank groups), then one TMA tensor store writes 16 full 128-byte rows.
-// Two tiles per warp alternate; a tile is reused once its store has read it.
-template <int NT = 2>  // output tiles per warp (1: the store must have read it first)
+// NT = 2: two tiles per warp alternate (SIMD-BP128, whose short iterations
+// need the overlap); NT = 1: the page decoders, whose long iterations hide
+// the wait and whose exception loads want the shared memory back as L1.
+// A tile is reused once its store has read it.
+template <int NT = 2>
 struct OutStageT {
   static constexpr bool kProbe = false;  // see ProbeStage (probe.cuh)
   static constexpr bool kAgg = false;    // see AggStage (split.cuh)
