@@ -2,15 +2,25 @@
 """Benchmark: fused SIMD-BP128+D4 and SIMD-FastPFOR+D4 decode on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c5|c1|c4]
+                    [--workload c5|c1|c4] [--arrays M] [--dry-run]
 
 Workload (default c5 = BASELINE.json configs[4], the config the metric is
 quoted on at 1/2/4/8 GPUs): 65,536 arrays x 65,536 sorted distinct uint32 from
 the seeded BASELINE ClusterData recipe, d ~ U{20..29} per array, encoded with
-simdbp128-s4 AND simdfastpfor-s4; arrays are partitioned by contiguous range
-across the N ranks (strong scaling, no data-path collective).  One step decodes
-the rank's shard under both codecs: one launch of the fused SIMD-BP128 kernel,
-then izg_decode_ws's two SIMD-FastPFOR launches (page index pass + decode).
+simdbp128-s4 AND simdfastpfor-s4.  Arrays are partitioned into contiguous
+ranges across the N ranks, balanced by the bytes each array moves (4 B per
+decoded integer plus the compressed size its d implies) — strong scaling, no
+data-path collective.  One step decodes the rank's shard under both codecs:
+one launch of the fused SIMD-BP128 kernel, then izg_decode_ws's two
+SIMD-FastPFOR launches (page index pass + decode).
+
+Ranks: one process per GPU.  Under torchrun (WORLD_SIZE set) the ranks come
+from the environment; `--gpus N` without WORLD_SIZE spawns the N ranks itself
+(RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* set per child) and fails loudly
+when fewer than N GPUs are visible — it never reports n_gpus: 1 for N > 1.
+Each rank binds its threads to the NUMA node of its GPU before allocating
+(first touch places its pinned host buffers there) and gets that node's
+cores divided by the ranks on it for input preparation.
 
 Timing: W warm-up steps, then K steps bracketed by a barrier and a device
 synchronize, measured with CUDA events on the launching stream; the max over
@@ -19,18 +29,26 @@ step dwarf the 126 MB L2, so no flush is needed.  After timing, every rank
 checksums its decoded output on the device and the mismatch count is
 sum-reduced over NCCL (the only collective).
 
-`e2e` repeats the metric through the host-buffer C ABI (izg_decode_host):
-pinned host words in, decoded integers back to pinned host memory, all copies
-inside the timed region.  `cpu_baseline` (rank 0, N=1) and `--impl reference`
-time the reference library itself (compiled from its sources into
-oracle/_ref) decoding a bounded sample of the same workload with every host
-thread.
+`e2e` repeats the metric over the same K steps through the host-buffer C ABI
+(izg_decode_host): pinned host words in, decoded integers back to pinned host
+memory, all copies inside the timed region.  `cpu_baseline` (rank 0, N=1)
+times the reference library itself (compiled from its sources into
+oracle/_ref) on a bounded sample with every host thread, and checks on that
+sample that the harness encoder's words equal the reference encoder's and
+that the GPU decodes the reference-encoded sample to the reference's output.
+
+`--impl reference` times the reference library on the FULL workload (same
+arrays, same codecs, same config keys) with every host thread.  That arm
+imports nothing from this repo's product or harness: its inputs come from the
+generator compiled into oracle/_ref (oracle/Makefile), its encoding and
+decoding are the reference's encode_array / decode_array.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -59,6 +77,15 @@ WORKLOADS = {
            "simdfastpfor-s4 (prefix sums wrap mod 2^32)"),
 }
 SEED = 20120910
+GEN_BATCH = 2048  # arrays generated per harness call
+
+
+def workload(args):
+    n, model, d, rate, codecs, desc = WORKLOADS[args.workload]
+    if args.arrays:
+        n = min(n, args.arrays)
+        desc += f" [reduced to {n} arrays by --arrays]"
+    return n, model, d, rate, codecs, desc
 
 
 def peaks():
@@ -70,45 +97,163 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def dist_init():
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---- ranks -------------------------------------------------------------------
+
+def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    return world, rank, local, local_world
 
 
-def shard(n_arrays, world, rank):
-    lo = n_arrays * rank // world
-    hi = n_arrays * (rank + 1) // world
-    return lo, hi
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
-def build_inputs(P, wl, lo, hi, threads, want_values=False):
-    """Generate arrays [lo, hi) in batches, encode with every codec, return
-    per-codec Encoded (global out_off) plus the expected checksum."""
+def spawn_ranks(n: int, argv: list[str], dry_run: bool) -> int:
+    """`--gpus N` without a launcher: run N copies of this script as ranks
+    0..N-1 of one job (one process per GPU) and return the worst exit code."""
+    if not dry_run:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < n:
+            print(json.dumps({"error": f"--gpus {n} but only {have} CUDA device(s) visible"}),
+                  flush=True)
+            return 2
+    port = _free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *argv], env=env))
+    return max(p.wait() for p in procs)
+
+
+def numa_bind(local: int, local_world: int, pci: str | None):
+    """Pin this rank to the CPUs of its GPU's NUMA node (sysfs), so its pinned
+    host buffers are first-touched there; returns (prep threads, info)."""
+    info = {"node": None, "cpus": host_threads()}
+    cpus = None
+    if pci:
+        base = f"/sys/bus/pci/devices/{pci.lower()}"
+        try:
+            node = int(open(base + "/numa_node").read().strip())
+            info["node"] = node
+            if node >= 0:
+                lst = open(f"/sys/devices/system/node/node{node}/cpulist").read().strip()
+                cpus = set()
+                for part in lst.split(","):
+                    a, _, b = part.partition("-")
+                    cpus.update(range(int(a), int(b or a) + 1))
+        except (OSError, ValueError):
+            pass
+    if cpus:
+        try:
+            os.sched_setaffinity(0, cpus)
+            info["cpus"] = len(cpus)
+        except OSError:
+            pass
+    nodes = len([d for d in os.listdir("/sys/devices/system/node") if d.startswith("node")]) \
+        if os.path.isdir("/sys/devices/system/node") else 1
+    # ranks sharing this node share its cores (one GPU per rank, GPUs spread
+    # over the nodes; a single-node host gives every rank cores/ranks)
+    per_node = max(1, -(-local_world // max(nodes, 1))) if cpus else local_world
+    info["nodes"] = nodes
+    return max(1, info["cpus"] // per_node), info
+
+
+# ---- inputs ------------------------------------------------------------------
+
+def est_bytes_per_array(d: np.ndarray, n_codecs: int) -> np.ndarray:
+    """Bytes one array moves per step: 4 B per decoded integer per codec plus
+    the compressed size its d implies (measured: simdbp128-s4 + simdfastpfor-s4
+    take ~10.2 + 1.25 (d - 20) bits per integer together at d = 18..29)."""
+    bits = np.maximum(1.0, 10.2 + 1.25 * (d.astype(np.float64) - 20.0)) * n_codecs / 2
+    return N_INTS * (4.0 * n_codecs + bits / 8.0)
+
+
+def shard_weighted(weights: np.ndarray, world: int, rank: int):
+    """Contiguous range [lo, hi) of rank `rank` cutting the prefix sum of
+    `weights` into `world` equal parts (every rank gets >= 1 array when there
+    are enough)."""
+    n = len(weights)
+    if world == 1:
+        return 0, n
+    cum = np.concatenate([[0.0], np.cumsum(weights)])
+    cuts = [0]
+    for r in range(1, world):
+        c = int(np.searchsorted(cum, cum[-1] * r / world))
+        cuts.append(min(max(c, cuts[-1]), n))
+    cuts.append(n)
+    return cuts[rank], cuts[rank + 1]
+
+
+def shard(n_arrays: int, world: int, rank: int):
+    """Equal array counts (used when every array weighs the same)."""
+    return n_arrays * rank // world, n_arrays * (rank + 1) // world
+
+
+def plan_shards(wl, world):
+    """Per-rank [lo, hi): byte-balanced by the per-array d (C5), count-balanced
+    where every array has the same shape (C1, C4)."""
+    import harness as H
+
+    n_arrays, model, d, _, codecs, _ = wl
+    if np.isscalar(d) or d[0] == d[1]:
+        return [shard(n_arrays, world, r) for r in range(world)]
+    w = est_bytes_per_array(H.array_widths(n_arrays, d, SEED), len(codecs))
+    return [shard_weighted(w, world, r) for r in range(world)]
+
+
+def build_inputs(wl, lo, hi, threads, want_values=False):
+    """Generate arrays [lo, hi) in batches (harness), host-encode with every
+    codec (word for word the reference encoder), return per-codec harness
+    Encoded (out_off relative to the shard) plus the expected checksum."""
+    import harness as H
+
     n_arrays, model, d, rate, codecs, _ = wl
-    batch = 2048
     enc_parts = {c: [] for c in codecs}
     word_base = {c: 0 for c in codecs}
-    ck = np.zeros(2, dtype=np.uint64)
     sums = [0, 0]
     values_keep = []
-    lib = P._native.lib()
-    for b0 in range(lo, hi, batch):
-        b1 = min(hi, b0 + batch)
+    for b0 in range(lo, hi, GEN_BATCH):
+        b1 = min(hi, b0 + GEN_BATCH)
         cnt = b1 - b0
-        vals, _ = P.gen_arrays(model, cnt, N_INTS, d, seed=SEED + b0, rate_ppm=rate,
+        vals, _ = H.gen_arrays(model, cnt, N_INTS, d, seed=SEED + b0, rate_ppm=rate,
                                threads=threads)
         flat = vals.reshape(-1)
-        lib.izg_checksum_host(P._native.ptr(flat), flat.size, (b0 - lo) * N_INTS, threads,
-                              P._native.ptr(ck))
-        sums[0] = (sums[0] + int(ck[0])) % (1 << 64)
-        sums[1] ^= int(ck[1])
+        s, x = H.checksum_host(flat, (b0 - lo) * N_INTS, threads)
+        sums[0] = (sums[0] + s) % (1 << 64)
+        sums[1] ^= x
         offs = np.arange(cnt, dtype=np.uint64) * N_INTS
         counts = np.full(cnt, N_INTS, dtype=np.uint32)
         for c in codecs:
-            e = P.encode_chunks(P.make_codec(c), flat, offs, counts,
-                                allow_wrap=(model == "geometric"), threads=threads)
+            e = H.encode_chunks(c, flat, offs, counts, allow_wrap=(model == "geometric"),
+                                threads=threads)
             e.table["word_off"] += np.uint64(word_base[c])
             e.table["out_off"] += np.uint64((b0 - lo) * N_INTS)
             word_base[c] += len(e.words)
@@ -118,9 +263,13 @@ def build_inputs(P, wl, lo, hi, threads, want_values=False):
         del vals, flat
     encs = {}
     for c in codecs:
-        words = np.concatenate([e.words for e in enc_parts[c]])
-        table = np.concatenate([e.table for e in enc_parts[c]])
-        encs[c] = P.Encoded(words, table)
+        if enc_parts[c]:
+            words = np.concatenate([e.words for e in enc_parts[c]])
+            table = np.concatenate([e.table for e in enc_parts[c]])
+        else:
+            words = np.zeros(4, np.uint32)
+            table = np.zeros(0, dtype=H.CHUNK_DTYPE)
+        encs[c] = H.Encoded(words, table)
     return encs, (sums[0], sums[1]), values_keep
 
 
@@ -191,68 +340,186 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_sample(wl, threads, budget_s=12.0, sample_arrays=None):
+# ---- the reference (CPU) -------------------------------------------------------
+
+def reference_batches(wl, first, count, threads, log=None):
     """The reference library (oracle/_ref, compiled from the reference's own
-    sources) decoding a bounded sample of the workload with `threads` host
-    threads: decode_array per array into pre-faulted per-array outputs."""
-    import paper_1209_2137_b200 as P
+    sources) holding arrays [first, first+count) of the workload, encoded by
+    the reference's encode_array (its wrapping variant for C4), ready for
+    timed decode_array passes into pre-faulted per-array outputs.  Inputs
+    come from the generator compiled into the same library (the harness
+    source), so nothing else from this repo is loaded.  Returns
+    ({codec: RefBatch}, expected checksum of the arrays)."""
     from oracle.pyoracle import Reference
 
     ref = Reference()
-    n_arrays, model, d, rate, codecs, _ = wl
-    m = sample_arrays or min(n_arrays, 1024)
-    vals, _ = P.gen_arrays(model, m, N_INTS, d, seed=SEED, rate_ppm=rate, threads=threads)
-    flat = vals.reshape(-1)
-    offs = np.arange(m, dtype=np.uint64) * N_INTS
-    counts = np.full(m, N_INTS, dtype=np.uint32)
-    batches = []
-    for c in codecs:
-        # encoded by the reference itself (encode_array; the wrapping variant
-        # for the C4 sums that exceed 2^32)
-        if model == "geometric":
-            payloads = [ref.encode_chunk_wrapping(c, vals[i]) for i in range(m)]
-        else:
-            payloads = [ref.encode_array(c, vals[i])[0][1] for i in range(m)]
-        e = P.layout(P.make_codec(c), payloads, counts)
-        b = ref.batch(c, e.words, e.table)
-        b.decode(threads=threads)  # warm-up + correctness
-        for i in (0, m - 1):
-            if not np.array_equal(b.output(i, N_INTS), vals[i]):
-                raise RuntimeError(f"reference decode mismatch on {c}")
-        batches.append(b)
-    return batches, m
+    _, model, d, rate, codecs, _ = wl
+    batches = {c: ref.batch_new(c) for c in codecs}
+    sums = [0, 0]
+    buf = None
+    for b0 in range(first, first + count, GEN_BATCH):
+        cnt = min(first + count, b0 + GEN_BATCH) - b0
+        if buf is None or buf.shape[0] != cnt:
+            buf = np.empty((cnt, N_INTS), dtype=np.uint32)
+        vals, _ = ref.gen_arrays(model, cnt, N_INTS, d, SEED + b0, rate_ppm=rate,
+                                 threads=threads, out=buf)
+        flat = vals.reshape(-1)
+        offs = np.arange(cnt, dtype=np.uint64) * N_INTS
+        counts = np.full(cnt, N_INTS, dtype=np.uint32)
+        for c in codecs:
+            batches[c].add(c, flat, offs, counts, wrap=(model == "geometric"), threads=threads)
+        # expected checksum of the whole range (numpy; the reference arm
+        # loads no repo library besides oracle/_ref)
+        v = flat.astype(np.uint64)
+        i = np.arange((b0 - first) * N_INTS, (b0 - first) * N_INTS + flat.size, dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            sums[0] = (sums[0] + int(np.sum((v + np.uint64(1)) * (np.uint64(2) * i + np.uint64(1)),
+                                            dtype=np.uint64))) % (1 << 64)
+        sums[1] ^= int(np.bitwise_xor.reduce(flat))
+        if log:
+            log(f"reference prep {b0 + cnt - first}/{count}")
+    return batches, (sums[0], sums[1])
 
 
 def run_reference_arm(args, wl, world, rank):
+    """--impl reference: the reference's decode_array over the FULL workload
+    (every array, every codec) per step on all host threads."""
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    batches, m = cpu_reference_sample(wl, threads)
-    ints = m * N_INTS * len(batches)
-    for _ in range(args.warmup):
-        for b in batches:
+    threads = host_threads()
+    n_arrays = wl[0]
+    t0 = time.time()
+    batches, expect = reference_batches(wl, 0, n_arrays, threads)
+    prep_s = time.time() - t0
+    # warm-up pass doubles as the correctness gate (every array, every codec)
+    verified = True
+    for c, b in batches.items():
+        b.decode(threads=threads)
+        if b.checksum() != expect:
+            verified = False
+    for _ in range(max(args.warmup - 1, 0)):
+        for b in batches.values():
             b.decode(threads=threads)
     times = []
     for _ in range(args.steps):
-        t = sum(b.decode(threads=threads) for b in batches)
-        times.append(t)
+        times.append(sum(b.decode(threads=threads) for b in batches.values()))
     tot = sum(times)
+    ints = n_arrays * N_INTS * len(batches)
     value = ints * args.steps / tot / 1e9
-    sample = (f"{m} of {wl[0]} arrays x {N_INTS} ints, {'+'.join(wl[4])}, one decode_array per "
-              f"array per step, {threads} threads")
+    bits = {c: round(32 * b.payload_words() / (n_arrays * N_INTS), 3) for c, b in batches.items()}
+    sample = (f"full workload: {n_arrays} arrays x {N_INTS} ints x {len(batches)} codecs per step, "
+              f"one decode_array per array into pre-faulted per-array outputs, {threads} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * tot / args.steps, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded BASELINE.json recipes; no dataset)",
-        "config": {"workload": wl[5], "sample": sample},
+        "config": {"workload": wl[5], "arrays": n_arrays, "ints_per_array": N_INTS,
+                   "codecs": list(batches), "bits_per_int": bits, "verified": verified,
+                   "prep_s": round(prep_s, 1)},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    if not verified:
+        sys.exit(1)
+
+
+def cpu_baseline_leg(wl, encs, threads, dev, budget_s=12.0, m=1024):
+    """rank 0, N = 1: the reference on a bounded sample (the first m arrays
+    of this rank's shard), plus two checks on that sample — the harness
+    encoder's words equal the reference encoder's, and the GPU decodes the
+    reference-encoded words to the reference's own output."""
+    import paper_1209_2137_b200 as P
+    from oracle.pyoracle import Reference
+
+    m = min(m, len(next(iter(encs.values())).table))
+    batches, expect = reference_batches(wl, 0, m, threads)
+    ref = Reference()
+    words_equal = gpu_equal = True
+    _, model, d, rate, codecs, _ = wl
+    vals, _ = ref.gen_arrays(model, m, N_INTS, d, SEED, rate_ppm=rate, threads=threads)
+    offs = np.arange(m, dtype=np.uint64) * N_INTS
+    counts = np.full(m, N_INTS, dtype=np.uint32)
+    for c in codecs:
+        rw, rt = ref.encode_batch(c, vals.reshape(-1), offs, counts,
+                                  wrap=(model == "geometric"), threads=threads)
+        e = encs[c]
+        hw = e.words[:int(e.table["word_off"][m - 1] + e.table["n_words"][m - 1])]
+        words_equal &= bool(np.array_equal(rw[:len(hw)], hw) and
+                            np.array_equal(rt["n_words"], e.table["n_words"][:m]))
+        b = P.DeviceBatch(P.make_codec(c), P.Encoded(rw, rt), dev)
+        b.decode()
+        b.check()
+        batches[c].decode(threads=threads)
+        gpu_equal &= b.checksum() == batches[c].checksum() == expect
+        del b
+    tt, reps, t_start = 0.0, 0, time.time()
+    while time.time() - t_start < budget_s and reps < 200:
+        tt += sum(b.decode(threads=threads) for b in batches.values())
+        reps += 1
+    cval = m * N_INTS * len(batches) * reps / tt / 1e9
+    return {"value": round(cval, 4), "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": f"first {m} arrays x {N_INTS} ints of this workload, {'+'.join(codecs)}, "
+                      f"{reps} passes of decode_array per array on {threads} threads "
+                      f"(reference compiled from source, oracle/_ref)",
+            "ref_encoder_words_equal_harness": words_equal,
+            "gpu_decodes_ref_encoded_sample": gpu_equal}
+
+
+def pcie_d2h_ceiling(dev, nbytes=1 << 30):
+    """Pinned device->host copy bandwidth (GB/s), best of 3: the ceiling of
+    the e2e number, which moves 4 B per decoded integer back to the host."""
+    import torch
+
+    src = torch.empty(nbytes // 4, dtype=torch.int32, device=dev)
+    dst = torch.empty(nbytes // 4, dtype=torch.int32, pin_memory=True)
+    best = 0.0
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize(dev)
+        best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+    del src, dst
+    return best
+
+
+# ---- our arm -------------------------------------------------------------------
+
+def run_dry(args, wl, world, rank):
+    """--dry-run: the rank plumbing without a GPU (gloo): shard plan, input
+    preparation and the reductions; the 'decode' is the generated input's own
+    checksum.  Used by tests/test_multirank.py."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    threads = max(1, host_threads() // max(1, world))
+    spans = plan_shards(wl, world)
+    lo, hi = spans[rank]
+    encs, expect, _ = build_inputs(wl, lo, hi, threads)
+    words = sum(e.payload_words for e in encs.values())
+    t = torch.tensor([float(words), float(hi - lo)], dtype=torch.float64)
+    allw = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(allw, t)
+    else:
+        allw = [t]
+    if rank == 0:
+        line = {"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "dry_run": True,
+                "config": {"workload": wl[5], "arrays": wl[0], "shards": spans,
+                           "payload_words_per_rank": [int(x[0].item()) for x in allw],
+                           "arrays_per_rank": [int(x[1].item()) for x in allw]}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -262,15 +529,27 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
-    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--arrays", type=int, default=0, help="reduce the workload (tests only)")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only, no GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    wl = WORKLOADS[args.workload]
-    world, rank, local = dist_init()
+    wl = workload(args)
 
     if args.impl == "reference":
-        run_reference_arm(args, wl, world, rank)
+        world = int(os.environ.get("WORLD_SIZE", args.gpus))
+        run_reference_arm(args, wl, world, int(os.environ.get("RANK", "0")))
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus, sys.argv[1:], args.dry_run))
+    world, rank, local, local_world = dist_env()
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} disagrees with WORLD_SIZE={world}"}),
+              flush=True)
+        sys.exit(2)
+    if args.dry_run:
+        run_dry(args, wl, world, rank)
         return
 
     import torch
@@ -279,20 +558,22 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    props = torch.cuda.get_device_properties(dev)
+    pci = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+    threads, numa = numa_bind(local, local_world, pci)
     if world > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
-    threads = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE",
-                                                                          world))))
     n_arrays = wl[0]
-    lo, hi = shard(n_arrays, world, rank)
+    spans = plan_shards(wl, world)
+    lo, hi = spans[rank]
     t0 = time.time()
-    encs, expect, _ = build_inputs(P, wl, lo, hi, threads)
+    encs, expect, _ = build_inputs(wl, lo, hi, threads)
     prep_s = time.time() - t0
 
     # one output buffer shared by the codecs (each step rewrites it)
-    out = torch.empty(max(e.n_out for e in encs.values()), dtype=torch.int32, device=dev)
+    out = torch.empty(max(max(e.n_out for e in encs.values()), 1), dtype=torch.int32, device=dev)
     batches = {c: P.DeviceBatch(P.make_codec(c), encs[c], dev, out=out) for c in wl[4]}
     stream = torch.cuda.current_stream(dev)
 
@@ -301,7 +582,7 @@ def main():
             torch.distributed.barrier()
 
     def step(events=None):
-        for i, (c, b) in enumerate(batches.items()):
+        for c, b in batches.items():
             if events is not None:
                 events[c][0].record(stream)
             b.decode(stream)
@@ -315,7 +596,7 @@ def main():
         b.check()
 
     kev = {c: [] for c in batches}
-    clocks = ClockSampler(torch.cuda.current_device())
+    clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     barrier()
@@ -345,15 +626,18 @@ def main():
         b.check()
         if b.checksum() != expect:
             mism += 1
-    t_el = torch.tensor([elapsed, float(mism)], dtype=torch.float64, device=dev)
+    my_words = sum(e.payload_words for e in encs.values())
+    t_el = torch.tensor([elapsed, float(mism), float(my_words), float(hi - lo)],
+                        dtype=torch.float64, device=dev)
+    per_rank_words = [my_words]
     if world > 1:
         import torch.distributed as dist
 
-        mx = t_el[:1].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t_el[1:].clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        elapsed, mism = float(mx.item()), int(sm.item())
+        gathered = [torch.zeros_like(t_el) for _ in range(world)]
+        dist.all_gather(gathered, t_el)
+        elapsed = max(float(g[0].item()) for g in gathered)
+        mism = int(sum(g[1].item() for g in gathered))
+        per_rank_words = [int(g[2].item()) for g in gathered]
 
     total_ints = n_arrays * N_INTS * len(batches)  # whole job, all ranks
     value = total_ints * args.steps / elapsed / 1e9
@@ -366,77 +650,79 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(args.workload, {}).get(dom)
-            traffic = tr
+            traffic = json.load(f).get(args.workload, {}).get(dom)
     except Exception:
         pass
 
-    # e2e through the host-buffer C ABI, pinned host memory, copies inside
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 3)
-    h_words = {}
-    h_tables = {}
-    h2d = d2h = 0
-    for c, e in encs.items():
-        hw = torch.empty(len(e.words), dtype=torch.int32, pin_memory=True)
-        hw.numpy().view(np.uint32)[:] = e.words
-        h_words[c] = hw
-        h_tables[c] = e.table
-        h2d += e.words.nbytes + e.table.nbytes
-        d2h += 4 * e.n_out + 4 * len(e.table)
-    n_out = max(e.n_out for e in encs.values())
-    h_out = torch.empty(n_out, dtype=torch.int32, pin_memory=True)
-    h_status = np.zeros(max(len(e.table) for e in encs.values()), dtype=np.int32)
-    lib = P._native.lib()
+    # e2e through the host-buffer C ABI, pinned host memory, copies inside,
+    # over the same K steps as `value`
+    e2e = None
+    if not args.no_e2e:
+        h_words, h_tables = {}, {}
+        h2d = d2h = 0
+        for c, e in encs.items():
+            hw = torch.empty(len(e.words), dtype=torch.int32, pin_memory=True)
+            hw.numpy().view(np.uint32)[:] = e.words
+            h_words[c] = hw
+            h_tables[c] = e.table
+            h2d += e.words.nbytes + e.table.nbytes
+            d2h += 4 * e.n_out + 4 * len(e.table)
+        n_out = max(max(e.n_out for e in encs.values()), 1)
+        h_out = torch.empty(n_out, dtype=torch.int32, pin_memory=True)
+        h_status = np.zeros(max(max(len(e.table) for e in encs.values()), 1), dtype=np.int32)
+        lib = P._native.lib()
 
-    def e2e_step():
-        for c in batches:
-            codec = P.make_codec(c)
-            rc = lib.izg_decode_host(codec.codec, codec.delta, h_words[c].data_ptr(),
-                                     len(encs[c].words), P._native.ptr(h_tables[c]),
-                                     len(h_tables[c]), h_out.data_ptr(), n_out,
-                                     P._native.ptr(h_status))
-            if rc != 0:
-                raise RuntimeError(f"izg_decode_host failed: {rc}")
+        def e2e_step():
+            for c in batches:
+                codec = P.make_codec(c)
+                rc = lib.izg_decode_host(codec.codec, codec.delta, h_words[c].data_ptr(),
+                                         len(encs[c].words), P._native.ptr(h_tables[c]),
+                                         len(h_tables[c]), h_out.data_ptr(), n_out,
+                                         P._native.ptr(h_status))
+                if rc != 0:
+                    raise RuntimeError(f"izg_decode_host failed: {rc}")
 
-    e2e_step()  # warm-up (scratch allocation)
-    barrier()
-    te = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
-    te = time.perf_counter() - te
-    if world > 1:
-        import torch.distributed as dist
+        e2e_step()  # warm-up (scratch allocation)
+        barrier()
+        te = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        te = time.perf_counter() - te
+        if world > 1:
+            import torch.distributed as dist
 
-        t = torch.tensor([te], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        te = float(t.item())
-    e2e_value = total_ints * e2e_steps / te / 1e9
-    # last e2e step's output must equal the last codec's decode
-    last = list(batches)[-1]
-    ck = np.zeros(2, dtype=np.uint64)
-    lib.izg_checksum_host(h_out.data_ptr(), encs[last].n_out, 0, threads, P._native.ptr(ck))
-    e2e_ok = (int(ck[0]), int(ck[1])) == expect
+            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        import harness as H
+
+        last = list(batches)[-1]
+        e2e_ok = H.checksum_host(h_out.numpy(), 0, threads) == expect if encs[last].n_out else True
+        ceiling_gbs = pcie_d2h_ceiling(dev)
+        bytes_per_int = (h2d + d2h) / max(1, sum(e.n_out for e in encs.values()))
+        e2e = {"value": round(total_ints * args.steps / te / 1e9, 3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": args.steps,
+               "path": "izg_decode_host (pinned host buffers; H2D + decode on 4 slot streams, "
+                       "D2H split over 3 streams)",
+               "verified": e2e_ok,
+               "pcie_d2h_gbs_rank0": round(ceiling_gbs, 1),
+               "ceiling_note": (f"host-buffer decode moves 4 B per decoded integer over the "
+                                f"rank's own PCIe link (measured D2H {ceiling_gbs:.1f} GB/s): "
+                                f"<= {ceiling_gbs / 4:.1f} G int/s per GPU whatever the kernels "
+                                f"do, so at N=1 e2e can at best tie a 16-core host; every added "
+                                f"GPU adds a link")}
+        del h_words, h_out
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cthreads = os.cpu_count() or 1
-            cb, m = cpu_reference_sample(wl, cthreads)
-            tt, reps, t_start = 0.0, 0, time.time()
-            while time.time() - t_start < 12.0 and reps < 200:
-                tt += sum(b.decode(threads=cthreads) for b in cb)
-                reps += 1
-            cval = m * N_INTS * len(cb) * reps / tt / 1e9
-            cpu = {"value": round(cval, 4), "unit": UNIT, "cores": cthreads, "kind": "reference",
-                   "sample": f"{m} arrays x {N_INTS} ints of this workload, {'+'.join(wl[4])}, "
-                             f"{reps} passes of decode_array per array on {cthreads} threads "
-                             f"(reference compiled from source, oracle/_ref)"}
+            cpu = cpu_baseline_leg(wl, encs, host_threads(), dev)
         except Exception as ex:  # reference library absent on this box
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
 
     if rank == 0:
-        bits = {c: round(32 * encs[c].payload_words / ((hi - lo) * N_INTS), 3) for c in encs}
+        bits = {c: round(32 * encs[c].payload_words / max(1, (hi - lo) * N_INTS), 3) for c in encs}
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -445,11 +731,15 @@ def main():
             "dtype": "u32", "data": "synthetic (seeded BASELINE.json recipes; no dataset)",
             "config": {
                 "workload": wl[5], "arrays": n_arrays, "ints_per_array": N_INTS,
-                "codecs": list(batches), "bits_per_int_rank0": bits,
+                "codecs": list(batches), "bits_per_int": bits,
                 "ms_per_launch_rank0": {c: round(v, 4) for c, v in kern_ms.items()},
                 "l2": "inputs+outputs per step >> 126 MB L2 (no flush needed)",
-                "parallelism": f"shard by array over {world} rank(s); NCCL only for the "
-                               "final checksum and timing reduction",
+                "parallelism": f"shard by array over {world} rank(s), contiguous ranges "
+                               "balanced by bytes moved; NCCL only for the final checksum "
+                               "and timing reduction",
+                "shards": spans if world > 1 else None,
+                "payload_words_per_rank": per_rank_words,
+                "numa_rank0": numa, "prep_threads_rank0": threads,
                 "verified": mism == 0, "prep_s_rank0": round(prep_s, 1),
             },
             "roofline": {"bound": "hbm",
@@ -461,10 +751,7 @@ def main():
                          "traffic": traffic,
                          "algorithmic_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                    "path": "izg_decode_host (pinned host buffers; H2D + decode on 4 slot streams, D2H split over 3 streams)",
-                    "verified": e2e_ok},
+            "e2e": e2e,
             "clocks": clk,
             "gpu_launches": args.steps * sum(b.launches_per_decode for b in batches.values()),
         }

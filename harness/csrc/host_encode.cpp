@@ -1,6 +1,6 @@
-// host_encode.cpp — host-side mirror of the reference's encode path for the
-// hot-path codecs, used to produce device inputs (bench.py, tests) and as
-// the CPU half of "CPU-encoded buffers decode on the GPU".
+// host_encode.cpp — host encoder for the hot-path codecs (bench/test
+// HARNESS, libizh.so; not in the product library): produces device inputs
+// for bench.py and the tests, word-for-word equal to the reference encoder.
 //
 // Restates, word-level and multithreaded over chunks:
 //   encode_array                      codec.cpp:14-37
@@ -18,10 +18,9 @@
 #include <thread>
 #include <vector>
 
-#include "../../include/intzip_b200.h"
-#include "intzip_b200_host.h"
+#include "izh.h"
 
-namespace izg {
+namespace izh {
 namespace {
 
 inline uint32_t bit_width(uint32_t v) { return v ? 32u - (uint32_t)__builtin_clz(v) : 0u; }
@@ -202,6 +201,21 @@ void vbyte_append(const uint32_t* v, size_t n, std::vector<uint32_t>& out) {
 
 }  // namespace
 
+// Placement of izg_layout_chunks (include/intzip_b200.h): SIMD-BP128
+// payloads start on a 16-byte boundary, SIMD-FastPFOR pages at 12 mod 16 so
+// that their packed rows (word 1 + 4k) are 16-byte aligned; returns the
+// buffer size in words (whole 16-byte rows plus one spare row).
+uint64_t place(int codec, const uint32_t* n_words, uint32_t n_chunks, uint64_t* off) {
+  const uint64_t phase = codec == IZG_SIMDFASTPFOR ? 3 : 0;
+  uint64_t pos = phase;
+  for (uint32_t i = 0; i < n_chunks; ++i) {
+    pos += (phase - pos) & 3;  // next word at `phase` mod 4
+    off[i] = pos;
+    pos += n_words[i];
+  }
+  return (pos + 3) / 4 * 4 + 4;
+}
+
 // One chunk of encode_array; returns false on a decreasing input (no wrap).
 bool encode_chunk(int codec, int delta, const uint32_t* values, uint32_t n, bool wrap,
                   std::vector<uint32_t>& scratch, std::vector<uint32_t>& out) {
@@ -216,11 +230,11 @@ bool encode_chunk(int codec, int delta, const uint32_t* values, uint32_t n, bool
   return true;
 }
 
-}  // namespace izg
+}  // namespace izh
 
 // ---- C ABI -----------------------------------------------------------------
 
-struct izg_encoded {
+struct izh_encoded {
   std::vector<std::vector<uint32_t>> payloads;
   std::vector<izg_chunk> table;
   std::vector<uint64_t> offs;
@@ -228,7 +242,7 @@ struct izg_encoded {
   int codec = 0;
 };
 
-extern "C" izg_encoded* izg_encode_batch_host(int codec, int delta, const uint32_t* values,
+extern "C" izh_encoded* izh_encode_batch(int codec, int delta, const uint32_t* values,
                                               const uint64_t* value_off, const uint32_t* counts,
                                               uint32_t n_chunks, int allow_wrap, int threads,
                                               int* status) {
@@ -247,7 +261,7 @@ extern "C" izg_encoded* izg_encode_batch_host(int codec, int delta, const uint32
       return nullptr;
     }
   }
-  auto* e = new izg_encoded;
+  auto* e = new izh_encoded;
   e->codec = codec;
   e->payloads.resize(n_chunks);
   std::vector<int> bad(std::max(threads, 1), 0);
@@ -256,7 +270,7 @@ extern "C" izg_encoded* izg_encode_batch_host(int codec, int delta, const uint32
     for (uint32_t i = lo; i < hi; ++i) {
       auto& out = e->payloads[i];
       out.reserve(counts[i] / 2 + 64);
-      if (!izg::encode_chunk(codec, delta, values + value_off[i], counts[i], allow_wrap != 0,
+      if (!izh::encode_chunk(codec, delta, values + value_off[i], counts[i], allow_wrap != 0,
                              scratch, out))
         bad[t] = 1;
     }
@@ -283,16 +297,16 @@ extern "C" izg_encoded* izg_encode_batch_host(int codec, int delta, const uint32
   std::vector<uint32_t> sizes(n_chunks);
   for (uint32_t i = 0; i < n_chunks; ++i) sizes[i] = (uint32_t)e->payloads[i].size();
   e->offs.resize(n_chunks);
-  e->total_words = izg_layout_chunks(codec, sizes.data(), n_chunks, e->offs.data());
+  e->total_words = izh::place(codec, sizes.data(), n_chunks, e->offs.data());
   e->table.resize(n_chunks);
   for (uint32_t i = 0; i < n_chunks; ++i)
     e->table[i] = izg_chunk{e->offs[i], sizes[i], counts[i], value_off[i]};
   return e;
 }
 
-extern "C" uint64_t izg_encoded_words(const izg_encoded* e) { return e ? e->total_words : 0; }
+extern "C" uint64_t izh_encoded_words(const izh_encoded* e) { return e ? e->total_words : 0; }
 
-extern "C" int izg_encoded_copy(const izg_encoded* e, uint32_t* words, izg_chunk* table,
+extern "C" int izh_encoded_copy(const izh_encoded* e, uint32_t* words, izg_chunk* table,
                                 int threads) {
   if (!e) return IZG_ERR_INVALID_ARGUMENT;
   const uint32_t n = (uint32_t)e->payloads.size();
@@ -322,4 +336,4 @@ extern "C" int izg_encoded_copy(const izg_encoded* e, uint32_t* words, izg_chunk
   return IZG_SUCCESS;
 }
 
-extern "C" void izg_encoded_free(izg_encoded* e) { delete e; }
+extern "C" void izh_encoded_free(izh_encoded* e) { delete e; }

@@ -234,6 +234,28 @@ class Reference:
         L.izr_batch_output.argtypes = [vp, u32, vp]
         L.izr_batch_free.restype = None
         L.izr_batch_free.argtypes = [vp]
+        L.izr_batch_new.restype = vp
+        L.izr_batch_new.argtypes = [cp]
+        L.izr_batch_adopt.restype = None
+        L.izr_batch_adopt.argtypes = [vp, vp, C.c_int]
+        L.izr_batch_size.restype = u32
+        L.izr_batch_size.argtypes = [vp]
+        L.izr_batch_payload_words.restype = u64
+        L.izr_batch_payload_words.argtypes = [vp]
+        L.izr_batch_checksum.restype = None
+        L.izr_batch_checksum.argtypes = [vp, u32, u32, u64, vp]
+        L.izr_encode_batch.restype = vp
+        L.izr_encode_batch.argtypes = [cp, vp, vp, vp, u32, C.c_int, C.c_int, C.c_char_p,
+                                       C.c_int]
+        L.izr_encoded_size.restype = None
+        L.izr_encoded_size.argtypes = [vp, C.c_int, C.POINTER(u64), C.POINTER(u32)]
+        L.izr_encoded_copy.restype = None
+        L.izr_encoded_copy.argtypes = [vp, C.c_int, vp, vp]
+        L.izr_encoded_free.restype = None
+        L.izr_encoded_free.argtypes = [vp]
+        # the bench/test input generator (harness/csrc/datagen.cpp) compiled in
+        L.izh_gen_arrays.restype = C.c_int
+        L.izh_gen_arrays.argtypes = [C.c_int, u32, u32, u32, u32, u64, u32, C.c_int, vp, vp]
         L.izr_container_write_encoded.restype = C.c_int
         L.izr_container_write_encoded.argtypes = [cp, vp, vp, vp, u32, vp, u64, C.POINTER(u64),
                                                   C.c_char_p, C.c_int]
@@ -444,6 +466,52 @@ class Reference:
             raise RefError(2, "gen")
         return out[:n]
 
+    # ---- harness generator compiled into the shim (reference arm inputs) ----
+    def gen_arrays(self, model, count, n, d, seed, *, rate_ppm=0, threads=1, out=None):
+        """Same arrays as harness.gen_arrays (the same source, datagen.cpp)."""
+        d_lo, d_hi = (d, d) if np.isscalar(d) else d
+        if out is None:
+            out = np.empty((count, n), dtype=np.uint32)
+        dd = np.empty(count, dtype=np.uint32)
+        models = {"uniform": 0, "cluster": 1, "geometric": 2, "raw": 3}
+        if self.L.izh_gen_arrays(models[model], count, n, d_lo, d_hi, seed, rate_ppm, threads,
+                                 _p(out), _p(dd)):
+            raise RefError(2, "gen_arrays: bad arguments")
+        return out, dd
+
+    # ---- threaded batch encode with the reference encoder ----
+    def _encode_handle(self, name, values, value_off, counts, wrap, threads):
+        values = np.ascontiguousarray(values, dtype=np.uint32)
+        value_off = np.ascontiguousarray(value_off, dtype=np.uint64)
+        counts = np.ascontiguousarray(counts, dtype=np.uint32)
+        err = C.create_string_buffer(256)
+        h = self.L.izr_encode_batch(name.encode(), _p(values), _p(value_off), _p(counts),
+                                    len(counts), int(wrap), threads, err, 256)
+        if not h:
+            raise RefError(2, err.value.decode())
+        return h
+
+    def encode_batch(self, name, values, value_off, counts, *, wrap=False, threads=1, phase=None):
+        """Arrays values[value_off[i]:+counts[i]] through encode_array (or the
+        wrapping rule, wrap=True), on `threads` threads.  Returns (words,
+        table): chunk payloads placed with word 0 at `phase` mod 4 (default:
+        izg_layout_chunks' placement for the codec), outputs back to back."""
+        if phase is None:
+            phase = 3 if name.startswith("simdfastpfor") else 0
+        h = self._encode_handle(name, values, value_off, counts, wrap, threads)
+        try:
+            nw, nc = C.c_uint64(), C.c_uint32()
+            self.L.izr_encoded_size(h, phase, C.byref(nw), C.byref(nc))
+            words = np.empty(nw.value, dtype=np.uint32)
+            table = np.empty(nc.value, dtype=CHUNK_DTYPE)
+            self.L.izr_encoded_copy(h, phase, _p(words), _p(table))
+        finally:
+            self.L.izr_encoded_free(h)
+        return words, table
+
+    def batch_new(self, name):
+        return RefBatch(self, self.L.izr_batch_new(name.encode()), 0)
+
     # ---- timed batch decode (reference arm / cpu_baseline) ----
     def batch(self, name, words, table):
         words = np.ascontiguousarray(words, dtype=np.uint32)
@@ -455,6 +523,21 @@ class Reference:
 class RefBatch:
     def __init__(self, ref, handle, n):
         self.ref, self.h, self.n = ref, handle, n
+
+    def add(self, name, values, value_off, counts, *, wrap=False, threads=1):
+        """Encode arrays with the reference (threaded) and append them."""
+        h = self.ref._encode_handle(name, values, value_off, counts, wrap, threads)
+        self.ref.L.izr_batch_adopt(self.h, h, threads)
+        self.n = self.ref.L.izr_batch_size(self.h)
+
+    def payload_words(self) -> int:
+        return int(self.ref.L.izr_batch_payload_words(self.h))
+
+    def checksum(self, first=0, count=None, base=0):
+        count = self.n - first if count is None else count
+        out = np.zeros(2, dtype=np.uint64)
+        self.ref.L.izr_batch_checksum(self.h, first, count, base, _p(out))
+        return int(out[0]), int(out[1])
 
     def decode(self, first=0, count=None, threads=1) -> float:
         count = self.n - first if count is None else count

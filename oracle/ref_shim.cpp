@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -237,32 +238,187 @@ int izr_gen(int model, uint64_t n, uint64_t range, uint64_t seed, uint32_t* out)
   });
 }
 
+// ---- threaded batch encode with the reference encoder -------------------
+//
+// Entry i is one array values[value_off[i] .. + counts[i]) encoded by
+// intzip::encode_array (codec.cpp:14-37), or — wrap != 0, arrays of at most
+// one chunk — by the izr_encode_chunk_wrapping rule above (C4's wrapped
+// inputs).  Arrays are encoded on `threads` threads; all the coding work is
+// the reference's.
+struct Encoded {
+  std::vector<std::vector<intzip::Chunk>> arrays;
+};
+
+}  // extern "C"
+
+namespace {
+
+std::vector<intzip::Chunk> encode_one(const intzip::Codec& codec, const uint32_t* v, uint32_t n,
+                                      bool wrap) {
+  if (!wrap) return intzip::encode_array(codec, {v, n});
+  if (n == 0 || n > intzip::kChunkSize) throw std::invalid_argument("wrap: bad n");
+  std::vector<uint32_t> d(v, v + n);
+  const size_t stride = codec.delta_mode() == intzip::DeltaMode::stride4 ? 4 : 1;
+  for (size_t i = d.size(); i-- > stride;) d[i] -= d[i - stride];
+  const size_t core = n / codec.block_multiple() * codec.block_multiple();
+  intzip::Chunk c;
+  c.original_length = n;
+  codec.encode_deltas(d.data(), core, c.payload);
+  if (core < n) {
+    std::vector<uint8_t> rem;
+    intzip::vbyte_encode({d.data() + core, n - core}, rem);
+    intzip::append_bytes_as_words(rem, c.payload);
+  }
+  return {std::move(c)};
+}
+
+template <class F>
+void ranges(uint32_t count, int threads, F&& f) {
+  threads = std::max(1, std::min<int>(threads, (int)std::max<uint32_t>(count, 1)));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    const uint32_t lo = (uint64_t)count * t / threads, hi = (uint64_t)count * (t + 1) / threads;
+    if (lo < hi) pool.emplace_back(f, lo, hi);
+  }
+  for (auto& th : pool) th.join();
+}
+
+// First word of every chunk at `phase` mod 4 (phase < 0: back to back).
+uint64_t place(const Encoded& e, int phase, ChunkRec* table) {
+  uint64_t pos = phase < 0 ? 0 : (uint64_t)phase, out = 0;
+  uint32_t k = 0;
+  for (const auto& a : e.arrays)
+    for (const auto& c : a) {
+      if (phase >= 0) pos += ((uint64_t)phase - pos) & 3;
+      if (table) table[k] = {pos, (uint32_t)c.payload.size(), c.original_length, out};
+      ++k;
+      pos += c.payload.size();
+      out += c.original_length;
+    }
+  return (pos + 3) / 4 * 4 + 4;
+}
+
+}  // namespace
+
+extern "C" {
+
+void* izr_encode_batch(const char* name, const uint32_t* values, const uint64_t* value_off,
+                       const uint32_t* counts, uint32_t n_arrays, int wrap, int threads,
+                       char* err, int errcap) {
+  auto* e = new Encoded;
+  const int rc = guarded(err, errcap, [&] {
+    const auto codec = intzip::make_codec(name);
+    e->arrays.resize(n_arrays);
+    std::atomic<int> failed{0};
+    std::string what;
+    std::mutex mu;
+    ranges(n_arrays, threads, [&](uint32_t lo, uint32_t hi) {
+      for (uint32_t i = lo; i < hi && !failed; ++i) {
+        try {
+          e->arrays[i] = encode_one(*codec, values + value_off[i], counts[i], wrap != 0);
+        } catch (const std::exception& x) {
+          std::lock_guard<std::mutex> g(mu);
+          if (!failed.exchange(1)) what = x.what();
+        }
+      }
+    });
+    if (failed) throw std::invalid_argument(what);
+  });
+  if (rc) {
+    delete e;
+    return nullptr;
+  }
+  return e;
+}
+
+// Sizes of the placed words buffer and of the chunk table.
+void izr_encoded_size(void* h, int phase, uint64_t* n_words, uint32_t* n_chunks) {
+  const auto* e = static_cast<Encoded*>(h);
+  uint32_t k = 0;
+  for (const auto& a : e->arrays) k += (uint32_t)a.size();
+  *n_chunks = k;
+  *n_words = place(*e, phase, nullptr);
+}
+
+// Copy out the payloads (placed, gaps zero) and the chunk table.
+void izr_encoded_copy(void* h, int phase, uint32_t* words, ChunkRec* table) {
+  const auto* e = static_cast<Encoded*>(h);
+  const uint64_t total = place(*e, phase, table);
+  std::memset(words, 0, total * 4);
+  uint32_t k = 0;
+  for (const auto& a : e->arrays)
+    for (const auto& c : a) {
+      std::memcpy(words + table[k].word_off, c.payload.data(), c.payload.size() * 4);
+      ++k;
+    }
+}
+
+void izr_encoded_free(void* h) { delete static_cast<Encoded*>(h); }
+
 // ---- timed batch decode: the reference arm / cpu_baseline --------------
 //
-// Each table entry is one array of one chunk (every config uses 65,536-int
-// arrays).  The batch owns intzip::Chunk objects and one output vector per
-// array, so a timed pass is exactly `decode_array(codec, {chunk}, out_i)`
+// A batch holds arrays of intzip::Chunk objects and one output vector per
+// array, so a timed pass is exactly `decode_array(codec, chunks_i, out_i)`
 // per array (codec.cpp:39-69) into pre-faulted, reused per-array outputs,
 // spread over T threads in contiguous ranges (number 1).
 struct Batch {
   std::unique_ptr<intzip::Codec> codec;
-  std::vector<intzip::Chunk> chunks;
+  std::vector<std::vector<intzip::Chunk>> arrays;
   std::vector<std::vector<uint32_t>> outs;
 };
 
+// Each table entry is its own array of one chunk.
 void* izr_batch_create(const char* name, const uint32_t* words,
                        const ChunkRec* table, uint32_t n_chunks) {
   auto* b = new Batch;
   b->codec = intzip::make_codec(name);
-  b->chunks.resize(n_chunks);
+  b->arrays.resize(n_chunks);
   b->outs.resize(n_chunks);
   for (uint32_t i = 0; i < n_chunks; ++i) {
-    b->chunks[i].original_length = table[i].n;
-    b->chunks[i].payload.assign(words + table[i].word_off,
-                                words + table[i].word_off + table[i].n_words);
+    b->arrays[i].resize(1);
+    b->arrays[i][0].original_length = table[i].n;
+    b->arrays[i][0].payload.assign(words + table[i].word_off,
+                                   words + table[i].word_off + table[i].n_words);
     b->outs[i].assign(table[i].n, 0u);  // pre-fault
   }
   return b;
+}
+
+// Empty batch for `name`; arrays are appended with izr_batch_adopt.
+void* izr_batch_new(const char* name) {
+  auto* b = new Batch;
+  b->codec = intzip::make_codec(name);
+  return b;
+}
+
+// Move the arrays of an izr_encode_batch result into the batch (the handle
+// is consumed) and pre-fault their outputs on `threads` threads.
+void izr_batch_adopt(void* handle, void* enc, int threads) {
+  auto* b = static_cast<Batch*>(handle);
+  auto* e = static_cast<Encoded*>(enc);
+  const size_t first = b->arrays.size();
+  for (auto& a : e->arrays) b->arrays.push_back(std::move(a));
+  b->outs.resize(b->arrays.size());
+  delete e;
+  ranges((uint32_t)(b->arrays.size() - first), threads, [&](uint32_t lo, uint32_t hi) {
+    for (uint32_t i = lo; i < hi; ++i) {
+      size_t n = 0;
+      for (const auto& c : b->arrays[first + i]) n += c.original_length;
+      b->outs[first + i].assign(n, 0u);
+    }
+  });
+}
+
+uint32_t izr_batch_size(void* handle) {
+  return (uint32_t) static_cast<Batch*>(handle)->arrays.size();
+}
+
+// Compressed payload words of the whole batch.
+uint64_t izr_batch_payload_words(void* handle) {
+  uint64_t w = 0;
+  for (const auto& a : static_cast<Batch*>(handle)->arrays)
+    for (const auto& c : a) w += c.payload.size();
+  return w;
 }
 
 // One pass over `count` arrays starting at `first` on `threads` threads;
@@ -270,12 +426,12 @@ void* izr_batch_create(const char* name, const uint32_t* words,
 double izr_batch_decode(void* handle, uint32_t first, uint32_t count,
                         int threads) {
   auto* b = static_cast<Batch*>(handle);
-  if (first + count > b->chunks.size()) return -2.0;
+  if (first + count > b->arrays.size()) return -2.0;
   std::atomic<int> failed{0};
   auto work = [&](uint32_t lo, uint32_t hi) {
     for (uint32_t i = lo; i < hi; ++i) {
       try {
-        intzip::decode_array(*b->codec, {&b->chunks[i], 1}, b->outs[i]);
+        intzip::decode_array(*b->codec, b->arrays[i], b->outs[i]);
       } catch (...) {
         failed = 1;
       }
@@ -304,6 +460,22 @@ int izr_batch_output(void* handle, uint32_t i, uint32_t* out) {
   auto* b = static_cast<Batch*>(handle);
   std::memcpy(out, b->outs[i].data(), b->outs[i].size() * 4);
   return 0;
+}
+
+// Checksum (izh_checksum_host's definition) of arrays [first, first+count)
+// decoded back to back, the first integer having global index `base`.
+void izr_batch_checksum(void* handle, uint32_t first, uint32_t count, uint64_t base,
+                        uint64_t* out) {
+  auto* b = static_cast<Batch*>(handle);
+  uint64_t s = 0, x = 0, i = base;
+  for (uint32_t a = first; a < first + count; ++a)
+    for (uint32_t v : b->outs[a]) {
+      s += (uint64_t(v) + 1) * (2 * i + 1);
+      x ^= v;
+      ++i;
+    }
+  out[0] = s;
+  out[1] = x;
 }
 
 void izr_batch_free(void* handle) { delete static_cast<Batch*>(handle); }

@@ -5,8 +5,7 @@ include/intzip_b200.h; this package is its Python face (ctypes).
 """
 from . import _native
 from .codec import (CHUNK_SIZE, Codec, CorruptError, Encoded, codec_names, decode_array,
-                    encode_array, encode_chunks, gen_arrays, layout, make_codec,
-                    raise_for_status)
+                    encode_array, layout, make_codec, raise_for_status)
 from .container import (Container, decode_container, read_container, read_raw_container,
                         scan_container)
 from .device import DeviceBatch, decode_intersect_device, intersect, intersect_device
@@ -14,5 +13,5 @@ from .device import DeviceBatch, decode_intersect_device, intersect, intersect_d
 __all__ = ["CHUNK_SIZE", "Codec", "Container", "CorruptError", "DeviceBatch", "Encoded",
            "codec_names", "decode_container", "decode_intersect_device", "intersect", "intersect_device", "read_container", "read_raw_container",
            "scan_container",
-           "decode_array", "encode_array", "encode_chunks", "gen_arrays", "layout",
+           "decode_array", "encode_array", "layout",
            "make_codec", "raise_for_status", "_native"]

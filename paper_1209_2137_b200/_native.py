@@ -87,24 +87,10 @@ def lib() -> C.CDLL:
                                   C.c_uint64, vp]
     L.izg_release_host_scratch.restype = None
     L.izg_release_host_scratch.argtypes = []
-    L.izg_encode_batch_host.restype = vp
-    L.izg_encode_batch_host.argtypes = [C.c_int, C.c_int, vp, vp, vp, C.c_uint32, C.c_int,
-                                        C.c_int, C.POINTER(C.c_int)]
-    L.izg_encoded_words.restype = C.c_uint64
-    L.izg_encoded_words.argtypes = [vp]
-    L.izg_encoded_copy.restype = C.c_int
-    L.izg_encoded_copy.argtypes = [vp, vp, vp, C.c_int]
-    L.izg_encoded_free.restype = None
-    L.izg_encoded_free.argtypes = [vp]
-    L.izg_gen_arrays.restype = C.c_int
-    L.izg_gen_arrays.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
-                                 C.c_uint64, C.c_uint32, C.c_int, vp, vp]
     L.izg_encode.restype = C.c_int
     L.izg_encode.argtypes = [C.c_int, C.c_int, vp, vp, C.c_uint32, vp, vp, C.c_int, vp]
     L.izg_encode_bound.restype = C.c_uint64
     L.izg_encode_bound.argtypes = [C.c_int, C.c_uint32]
-    L.izg_checksum_host.restype = C.c_int
-    L.izg_checksum_host.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_int, vp]
     _lib = L
     return L
 

@@ -2,8 +2,9 @@
 
     python -m paper_1209_2137_b200.build [--force]
 
-The library holds the fused decode kernels, the C ABI of
-include/intzip_b200.h and the host helpers (encoder mirror, generators).
+The library holds the fused decode kernels, the GPU encoder and the C ABI of
+include/intzip_b200.h — nothing else (the bench/test input generators and
+host encoder live in harness/, a separate library).
 cudart is linked statically so the .so is self-contained on the GPU box.
 """
 from __future__ import annotations
@@ -20,10 +21,12 @@ LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libintzip_b200.so")
 OBJDIR = os.path.join(LIBDIR, "obj")
 
-SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "decode_split.cu", "decode_group.cu", "intersect.cu", "host.cpp", "host_encode.cpp",
-           "host_datagen.cpp", "container.cpp"]
+SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "decode_split.cu",
+           "decode_group.cu", "intersect.cu", "host.cpp", "container.cpp"]
 # per-source extra flags: see the comment at the top of decode_scalar.cu
 SOURCE_FLAGS = {"decode_scalar.cu": ["-Xptxas", "-O1"]}
+if os.environ.get("IZG_SCALAR_O1", "1") == "0":  # sanitizer repro builds only
+    SOURCE_FLAGS = {}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",

@@ -11,7 +11,6 @@ where it throws ``std::invalid_argument``.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -91,46 +90,22 @@ class Encoded:
         return int(self.table["n_words"].sum())
 
 
-def _threads() -> int:
-    return max(1, min(64, os.cpu_count() or 1))
+def encode_array(codec: Codec, values, *, allow_wrap: bool = False, device=None) -> Encoded:
+    """encode_array (codec.cpp:14-37) on the GPU encoder (izg_encode): chunks
+    of 2^16, delta, core, VByte tail.  Raises ValueError where the reference
+    throws std::invalid_argument (a decreasing input, delta.cpp:13)."""
+    from .device import encode_on_device
 
-
-def encode_chunks(codec: Codec, values: np.ndarray, value_off: np.ndarray,
-                  counts: np.ndarray, *, allow_wrap: bool = False, raw: bool = False,
-                  threads: int | None = None) -> Encoded:
-    """Host-encode independent chunks values[value_off[i] : +counts[i]].
-
-    raw=True encodes deltas as-is (Codec::encode_deltas, codec.h:31-34);
-    allow_wrap=True takes differences mod 2^32.
-    """
-    L = N.lib()
-    values = np.ascontiguousarray(values, dtype=np.uint32)
-    value_off = np.ascontiguousarray(value_off, dtype=np.uint64)
-    counts = np.ascontiguousarray(counts, dtype=np.uint32)
-    st = C.c_int()
-    delta = N.DELTA_NONE if raw else codec.delta
-    h = L.izg_encode_batch_host(codec.codec, delta, N.ptr(values), N.ptr(value_off),
-                                N.ptr(counts), len(counts), int(allow_wrap),
-                                threads or _threads(), C.byref(st))
-    if not h:
-        raise ValueError("encode: invalid input (decreasing values or bad counts)")
-    try:
-        nw = L.izg_encoded_words(h)
-        words = np.empty(nw, dtype=np.uint32)
-        table = np.empty(len(counts), dtype=CHUNK_DTYPE)
-        L.izg_encoded_copy(h, N.ptr(words), N.ptr(table), threads or _threads())
-    finally:
-        L.izg_encoded_free(h)
-    return Encoded(words, table)
-
-
-def encode_array(codec: Codec, values, *, allow_wrap: bool = False) -> Encoded:
-    """encode_array (codec.cpp:14-37): chunks of 2^16, delta, core, VByte tail."""
     values = np.ascontiguousarray(values, dtype=np.uint32)
     n = len(values)
     offs = np.arange(0, n, CHUNK_SIZE, dtype=np.uint64)
     counts = np.minimum(CHUNK_SIZE, n - offs).astype(np.uint32)
-    return encode_chunks(codec, values, offs, counts, allow_wrap=allow_wrap)
+    enc, status = encode_on_device(codec, values, offs, counts, allow_wrap=allow_wrap,
+                                   device=device)
+    bad = np.nonzero(status)[0]
+    if len(bad):
+        raise_for_status(int(status[bad[0]]), int(bad[0]))
+    return enc
 
 
 def layout(codec: Codec, payloads: list[np.ndarray], counts, out_offs=None) -> Encoded:
@@ -175,17 +150,3 @@ def decode_array(codec: Codec, enc: Encoded, *, raw: bool = False,
     if len(bad):
         raise_for_status(int(status[bad[0]]), int(bad[0]))
     return out[:n_out]
-
-
-def gen_arrays(model: str, count: int, n: int, d, seed: int, *, rate_ppm: int = 0,
-               threads: int | None = None):
-    """Seeded synthetic arrays (izg_gen_arrays); returns (values[count, n], d[count])."""
-    models = {"uniform": 0, "cluster": 1, "geometric": 2, "raw": 3}
-    d_lo, d_hi = (d, d) if np.isscalar(d) else d
-    out = np.empty((count, n), dtype=np.uint32)
-    dd = np.empty(count, dtype=np.uint32)
-    rc = N.lib().izg_gen_arrays(models[model], count, n, d_lo, d_hi, seed, rate_ppm,
-                                threads or _threads(), N.ptr(out), N.ptr(dd))
-    if rc != N.SUCCESS:
-        raise ValueError("gen_arrays: bad arguments")
-    return out, dd

@@ -36,11 +36,17 @@ __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) { return __ldg(p)
 // the fault vanished with any change to the loop (printf, no inlining, no
 // shared-memory ORs); plain ld.global is immune and costs nothing here.
 __device__ __forceinline__ uint32_t ld_u32(const uint32_t* p) {
+#ifdef IZG_PATCH_LDG  // sanitizer repro builds only
+  return __ldg(p);
+#endif
   uint32_t v;
   asm("ld.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
 __device__ __forceinline__ uint32_t ld_u8(const uint8_t* p) {
+#ifdef IZG_PATCH_LDG
+  return __ldg(p);
+#endif
   uint32_t v;
   asm("ld.global.u8 %0, [%1];" : "=r"(v) : "l"(p));
   return v;

@@ -14,8 +14,9 @@ def _ensure_built():
     lib = os.path.join(ROOT, "paper_1209_2137_b200", "_lib", "libintzip_b200.so")
     orc = os.path.join(ROOT, "oracle", "_build", "liboracle.so")
     ref = os.path.join(ROOT, "oracle", "_ref", "libintzip_ref.so")
+    hz = os.path.join(ROOT, "harness", "_build", "libizh.so")
     need_ref = not os.path.exists(ref) and os.path.isdir("/root/reference/proj/core")
-    if not os.path.exists(lib) or not os.path.exists(orc) or need_ref:
+    if not os.path.exists(lib) or not os.path.exists(orc) or not os.path.exists(hz) or need_ref:
         import __graft_entry__
 
         __graft_entry__.build()

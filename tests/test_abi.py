@@ -23,9 +23,42 @@ def test_exports_every_declared_symbol(native):
     lib = C.CDLL(N.LIB_PATH)
     names = declared(os.path.join(ROOT, "include", "intzip_b200.h"))
     assert set(N.ABI_SYMBOLS) <= set(names)
-    host = declared(os.path.join(ROOT, "paper_1209_2137_b200", "csrc", "intzip_b200_host.h"))
-    for name in names + host:
+    for name in names:
         assert hasattr(lib, name), name
+
+
+def test_product_library_exports_only_the_abi(native):
+    """The decoder .so exports the C ABI and nothing from the bench/test
+    harness (generators, host encoder: harness/libizh.so)."""
+    import shutil
+    import subprocess
+
+    nm = shutil.which("nm")
+    if not nm:
+        pytest.skip("nm not available")
+    out = subprocess.run([nm, "-D", "--defined-only", N.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    ours = {s for s in exported if s.startswith(("izg_", "izh_", "izr_"))}
+    names = set(declared(os.path.join(ROOT, "include", "intzip_b200.h")))
+    assert ours <= names, sorted(ours - names)
+    assert not any(s.startswith("izh_") for s in exported)
+
+
+def test_harness_placement_equals_layout_contract():
+    import harness as H
+
+    rng = np.random.default_rng(9)
+    for name, codec in (("simdbp128-s4", N.SIMDBP128), ("simdfastpfor-s4", N.SIMDFASTPFOR)):
+        lens = rng.integers(1, 70000, size=40).astype(np.uint64)
+        vals = np.sort(rng.integers(0, 2**31, size=int(lens.sum()), dtype=np.uint64)).astype(np.uint32)
+        offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+        counts = np.minimum(lens, 65536).astype(np.uint32)
+        enc = H.encode_chunks(name, vals, offs, counts)
+        sizes = enc.table["n_words"].copy()
+        woff = np.empty(len(sizes), np.uint64)
+        total = N.lib().izg_layout_chunks(codec, N.ptr(sizes), len(sizes), N.ptr(woff))
+        assert np.array_equal(woff, enc.table["word_off"]) and total == len(enc.words)
 
 
 def test_library_targets_sm100a(native):
@@ -108,9 +141,8 @@ def test_decode_argument_validation():
 
 
 def test_checksum_host_matches_numpy():
+    import harness as H
     from paper_1209_2137_b200.device import host_checksum
 
     v = np.random.default_rng(1).integers(0, 2**32, size=100003, dtype=np.uint64).astype(np.uint32)
-    out = np.zeros(2, np.uint64)
-    N.lib().izg_checksum_host(N.ptr(v), len(v), 17, 4, N.ptr(out))
-    assert (int(out[0]), int(out[1])) == host_checksum(v, 17)
+    assert H.checksum_host(v, 17, threads=4) == host_checksum(v, 17)

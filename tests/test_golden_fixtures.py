@@ -6,6 +6,7 @@ import os
 import numpy as np
 import pytest
 
+import harness as H
 import paper_1209_2137_b200 as P
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_vectors.npz")
@@ -50,7 +51,7 @@ def test_oracle_encodes_reference_vectors(oracle, gold):
 
 def test_host_encoder_reproduces_reference_vectors(native, gold):
     for name, vals, chunks in arrays(gold):
-        enc = P.encode_array(P.make_codec(name), vals)
+        enc = H.encode_array(P.make_codec(name), vals)
         for i, (_, p) in enumerate(chunks):
             t = enc.table[i]
             assert np.array_equal(enc.words[int(t["word_off"]):][:int(t["n_words"])], p), name

@@ -8,13 +8,14 @@ import numpy as np
 import pytest
 import torch
 
+import harness as H
 import paper_1209_2137_b200 as P
 
 pytestmark = pytest.mark.gpu
 
 
 def arrays(seed, k=6):
-    vals, _ = P.gen_arrays("cluster", k, 65536, 26, seed=seed)
+    vals, _ = H.gen_arrays("cluster", k, 65536, 26, seed=seed)
     return vals.reshape(-1)
 
 
@@ -25,7 +26,7 @@ def test_host_threads(cuda):
         codec = P.make_codec(name)
         flat = arrays(100 + i)
         if codec.codec in (0, 1):
-            enc = P.encode_array(codec, flat)
+            enc = H.encode_array(codec, flat)
         else:
             from oracle.pyoracle import Reference
 
@@ -56,7 +57,7 @@ def test_streams_race(cuda):
     batches, flats = [], []
     for i in range(4):
         flat = arrays(200 + i, k=16)
-        batches.append(P.DeviceBatch(codec, P.encode_array(codec, flat)))
+        batches.append(P.DeviceBatch(codec, H.encode_array(codec, flat)))
         flats.append(flat)
     streams = [torch.cuda.Stream() for _ in batches]
     for _ in range(5):

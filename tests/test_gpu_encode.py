@@ -5,6 +5,7 @@ import zlib
 import numpy as np
 import pytest
 
+import harness as H
 import paper_1209_2137_b200 as P
 from paper_1209_2137_b200.device import encode_on_device
 from tests.helpers import assorted_arrays, chunks_of, random_sorted
@@ -28,7 +29,7 @@ def test_gpu_encode_matches_host_encoder(cuda, name):
         offs, counts = _chunks(arr)
         genc, st = encode_on_device(codec, arr, offs, counts)
         assert np.all(st == 0)
-        henc = P.encode_chunks(codec, arr, offs, counts)
+        henc = H.encode_chunks(codec, arr, offs, counts)
         for (n1, a), (n2, b) in zip(chunks_of(genc), chunks_of(henc)):
             assert n1 == n2 and np.array_equal(a, b), (name, len(arr))
         assert np.array_equal(P.decode_array(codec, genc), arr)
@@ -71,7 +72,7 @@ def test_gpu_encode_raw_every_width(cuda, ref, codec_name):
 @pytest.mark.parametrize("name", ["simdbp128-s4", "simdfastpfor-s4"])
 def test_gpu_encode_wrap_and_decreasing(cuda, ref, name):
     codec = P.make_codec(name)
-    vals, _ = P.gen_arrays("geometric", 3, 65536, 32, seed=4, rate_ppm=50000)
+    vals, _ = H.gen_arrays("geometric", 3, 65536, 32, seed=4, rate_ppm=50000)
     flat = vals.reshape(-1)
     offs, counts = np.arange(3, dtype=np.uint64) * 65536, np.full(3, 65536, np.uint32)
     _, st = encode_on_device(codec, flat, offs, counts)
@@ -89,12 +90,12 @@ def test_gpu_encode_wrap_and_decreasing(cuda, ref, name):
 @pytest.mark.parametrize("name", ["simdbp128-s4", "simdfastpfor-s4"])
 def test_gpu_encode_large_batch_roundtrip(cuda, name):
     codec = P.make_codec(name)
-    vals, _ = P.gen_arrays("cluster", 512, 65536, (20, 29), seed=77)
+    vals, _ = H.gen_arrays("cluster", 512, 65536, (20, 29), seed=77)
     flat = vals.reshape(-1)
     offs, counts = np.arange(512, dtype=np.uint64) * 65536, np.full(512, 65536, np.uint32)
     genc, st = encode_on_device(codec, flat, offs, counts)
     assert np.all(st == 0)
-    henc = P.encode_chunks(codec, flat, offs, counts)
+    henc = H.encode_chunks(codec, flat, offs, counts)
     assert genc.payload_words == henc.payload_words
     b = P.DeviceBatch(codec, genc)
     b.decode()

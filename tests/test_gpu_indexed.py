@@ -14,6 +14,7 @@ import zlib
 import numpy as np
 import pytest
 
+import harness as H
 import paper_1209_2137_b200 as P
 from tests.helpers import random_sorted
 
@@ -88,7 +89,7 @@ def corpus(name, seed):
     payloads, counts = [], []
     for n in (128, 700, 2048 + 130, 9000, 65536):
         arr = outlier_array(rng, n)
-        p = P.encode_array(codec, arr)
+        p = H.encode_array(codec, arr)
         payload = p.words[int(p.table["word_off"][0]):][:int(p.table["n_words"][0])].copy()
         payloads.append(payload)
         counts.append(n)
@@ -174,7 +175,7 @@ def test_random_byte_fuzz_both_paths(cuda, name):
     for rep in range(400):
         n = int(rng.choice([300, 4096, 20000]))
         arr = outlier_array(rng, n) if rep % 2 else random_sorted(rng, n, 3000)
-        e = P.encode_array(codec, arr)
+        e = H.encode_array(codec, arr)
         p = e.words[int(e.table["word_off"][0]):][:int(e.table["n_words"][0])].copy()
         b = p.view(np.uint8)
         for _ in range(1 + rep % 3):
@@ -199,7 +200,7 @@ def test_workspace_too_small_falls_back_to_fused(cuda):
     codec = P.make_codec("simdfastpfor-s4")
     rng = np.random.default_rng(3)
     arr = outlier_array(rng, 3 * 65536)
-    enc = P.encode_array(codec, arr)
+    enc = H.encode_array(codec, arr)
     b = P.DeviceBatch(codec, enc, indexed=False)
     ws = torch.empty(64, dtype=torch.uint8, device="cuda")
     s = torch.cuda.current_stream()

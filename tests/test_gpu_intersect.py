@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 import torch
 
+import harness as H
 import paper_1209_2137_b200 as P
 from tests.helpers import random_sorted
 
@@ -56,7 +57,7 @@ def test_decode_then_intersect(cuda, name):
     a = random_sorted(rng, 200_000, 60)
     b = np.unique(np.concatenate([a[rng.random(len(a)) < 0.3],
                                   random_sorted(rng, 150_000, 80)])).astype(np.uint32)
-    got = P.intersect(codec, P.encode_array(codec, a), P.encode_array(codec, b))
+    got = P.intersect(codec, H.encode_array(codec, a), H.encode_array(codec, b))
     assert np.array_equal(got, np.intersect1d(a, b))
 
 
@@ -69,7 +70,7 @@ ALL_NAMES = ["simdbp128-s4", "simdbp128", "simdfastpfor-s4", "simdfastpfor", "bp
 def encode_any(name, flat):
     codec = P.make_codec(name)
     if codec.codec in (0, 1):
-        return codec, P.encode_array(codec, flat)
+        return codec, H.encode_array(codec, flat)
     from oracle.pyoracle import Reference
 
     ch = Reference().encode_array(name, flat)
@@ -139,7 +140,7 @@ def test_fused_several_arrays(cuda):
     flat = np.concatenate(arrs)
     counts = np.array([len(a) for a in arrs], np.uint32)
     offs = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
-    enc = P.encode_chunks(codec, flat, offs, counts)
+    enc = H.encode_chunks(codec, flat, offs, counts)
     s = np.unique(rng.integers(0, int(flat.max()) + 1, 20_000, dtype=np.uint32))
     b = P.DeviceBatch(codec, enc, materialize=False, indexed=False)
     got = P.decode_intersect_device(b, dev(s)).cpu().numpy().view(np.uint32)
@@ -152,7 +153,7 @@ def test_fused_status(cuda):
     rng = np.random.default_rng(8)
     long_ = random_sorted(rng, 65536 * 2, 40)
     codec = P.make_codec("simdbp128-s4")
-    enc = P.encode_array(codec, long_)
+    enc = H.encode_array(codec, long_)
     w = enc.words.copy()
     w[int(enc.table["word_off"][1])] = 0xFFFFFFFF  # widths > 32 in chunk 1
     from paper_1209_2137_b200.codec import Encoded
@@ -174,7 +175,7 @@ def test_intersect_fused_matches_unfused(cuda, name):
     a = random_sorted(rng, 300_000, 40)
     b = np.unique(np.concatenate([a[rng.random(len(a)) < 0.1],
                                   random_sorted(rng, 20_000, 600)])).astype(np.uint32)
-    ea, eb = P.encode_array(codec, a), P.encode_array(codec, b)
+    ea, eb = H.encode_array(codec, a), H.encode_array(codec, b)
     want = np.intersect1d(a, b)
     assert np.array_equal(P.intersect(codec, ea, eb, fused=True), want)
     assert np.array_equal(P.intersect(codec, ea, eb, fused=False), want)

@@ -8,6 +8,7 @@ import zlib
 import numpy as np
 import pytest
 
+import harness as H
 import paper_1209_2137_b200 as P
 from tests.helpers import (ALL_NAMES, REF_NAMES, assorted_arrays, chunks_of, misplace,
                            random_sorted)
@@ -19,7 +20,7 @@ pytestmark = pytest.mark.gpu
 def test_roundtrip_assorted(cuda, oracle, name):
     codec = P.make_codec(name)
     for arr in assorted_arrays(seed=zlib.crc32(name.encode()) % 1000):
-        enc = P.encode_array(codec, arr)
+        enc = H.encode_array(codec, arr)
         st, expect = oracle.decode_array(name, chunks_of(enc))
         assert st == 0 and np.array_equal(expect, arr)
         got = P.decode_array(codec, enc)
@@ -47,7 +48,7 @@ def test_unaligned_placement(cuda, name, word_phase, out_phase):
     rng = np.random.default_rng(word_phase * 7 + out_phase)
     arrs = [random_sorted(rng, n, 3000) for n in (70000, 300, 4096 + 5)]
     for arr in arrs:
-        enc = misplace(P.encode_array(codec, arr), word_phase, out_phase)
+        enc = misplace(H.encode_array(codec, arr), word_phase, out_phase)
         got = P.decode_array(codec, enc)
         assert np.array_equal(got[out_phase:], arr)
 
@@ -90,7 +91,7 @@ def test_device_batch_consumed_words(cuda, ref):
 
 def test_chunk_length_and_count_errors(cuda):
     codec = P.make_codec("simdbp128-s4")
-    enc = P.encode_array(codec, np.arange(1000, dtype=np.uint32))
+    enc = H.encode_array(codec, np.arange(1000, dtype=np.uint32))
     bad = P.Encoded(enc.words.copy(), enc.table.copy())
     bad.table["n"][0] = 0
     _, st = P.decode_array(codec, bad, return_status=True)
@@ -116,7 +117,7 @@ def test_mutation_fuzz_matches_oracle(cuda, oracle, name):
     payloads, counts = [], []
     for rep in range(300):
         arr = base_arrays[rep % 3]
-        p = chunks_of(P.encode_array(codec, arr))[0][1].copy()
+        p = chunks_of(H.encode_array(codec, arr))[0][1].copy()
         b = p.view(np.uint8)
         for _ in range(1 + rep % 4):
             b[rng.integers(0, len(b))] = rng.integers(0, 256)
@@ -170,10 +171,10 @@ def test_device_checksum_large_batch(cuda, name):
     from paper_1209_2137_b200.device import host_checksum
 
     codec = P.make_codec(name)
-    vals, _ = P.gen_arrays("cluster", 256, 65536, 29, seed=1234)
+    vals, _ = H.gen_arrays("cluster", 256, 65536, 29, seed=1234)
     flat = vals.reshape(-1)
     offs = np.arange(256, dtype=np.uint64) * 65536
-    enc = P.encode_chunks(codec, flat, offs, np.full(256, 65536, np.uint32))
+    enc = H.encode_chunks(codec, flat, offs, np.full(256, 65536, np.uint32))
     b = P.DeviceBatch(codec, enc)
     b.decode()
     b.check()

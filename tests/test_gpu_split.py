@@ -9,6 +9,7 @@ first error of a chunk in stream order travels with the look-back)."""
 import numpy as np
 import pytest
 
+import harness as H
 import paper_1209_2137_b200 as P
 from paper_1209_2137_b200 import _native as N
 from paper_1209_2137_b200.codec import Encoded
@@ -26,7 +27,7 @@ def batch_of(codec, arrays, allow_wrap=False):
     flat = np.concatenate(arrays).astype(np.uint32)
     counts = np.array([len(a) for a in arrays], np.uint32)
     offs = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
-    return flat, P.encode_chunks(codec, flat, offs, counts, allow_wrap=allow_wrap)
+    return flat, H.encode_chunks(codec, flat, offs, counts, allow_wrap=allow_wrap)
 
 
 def both(codec, enc, raw=False):
@@ -64,7 +65,7 @@ def test_split_arrays(cuda, name):
 def test_split_outliers(cuda, name):
     """C4-like pages: many exceptions, wrapping sums, every segment patched."""
     codec = P.make_codec(name)
-    vals, _ = P.gen_arrays("geometric", 6, 65536, 32, seed=5, rate_ppm=100000)
+    vals, _ = H.gen_arrays("geometric", 6, 65536, 32, seed=5, rate_ppm=100000)
     arrays = [v for v in vals] + [vals[0][:40000]]
     flat, enc = batch_of(codec, arrays, allow_wrap=True)
     s, o = both(codec, enc)
@@ -78,7 +79,7 @@ def test_split_multichunk_array(cuda):
     codec = P.make_codec("simdbp128-s4")
     rng = np.random.default_rng(1)
     flat = random_sorted(rng, 5 * 65536 + 777, 60)
-    enc = P.encode_array(codec, flat)
+    enc = H.encode_array(codec, flat)
     s, o = both(codec, enc)
     s.check()
     assert np.array_equal(s.output(), flat)
@@ -93,7 +94,7 @@ def test_split_raw(cuda, name):
     vals = (rng.integers(0, 1 << 32, int(counts.sum()), dtype=np.uint64)
             >> rng.integers(0, 32, int(counts.sum()), dtype=np.uint64)).astype(np.uint32)
     offs = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.uint64)
-    enc = P.encode_chunks(codec, vals, offs, counts, raw=True)
+    enc = H.encode_chunks(codec, vals, offs, counts, raw=True)
     s, o = both(codec, enc, raw=True)
     s.check()
     assert np.array_equal(s.output(), vals)
@@ -137,8 +138,8 @@ import numpy as np, paper_1209_2137_b200 as P
 for name, model, d, rate, count in [("simdbp128-s4", "cluster", 29, 0, 2048),
                                     ("simdfastpfor-s4", "geometric", 32, 100000, 1024)]:
     codec = P.make_codec(name)
-    vals, _ = P.gen_arrays(model, count, 65536, d, seed=1, rate_ppm=rate)
-    enc = P.encode_chunks(codec, vals.reshape(-1), np.arange(count, dtype=np.uint64) * 65536,
+    vals, _ = H.gen_arrays(model, count, 65536, d, seed=1, rate_ppm=rate)
+    enc = H.encode_chunks(codec, vals.reshape(-1), np.arange(count, dtype=np.uint64) * 65536,
                           np.full(count, 65536, np.uint32), allow_wrap=model == "geometric")
     b = P.DeviceBatch(codec, enc)
     for rep in range(3):

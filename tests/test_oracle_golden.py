@@ -4,6 +4,7 @@ library compiled from source where it is available."""
 import numpy as np
 import pytest
 
+import harness as H
 import paper_1209_2137_b200 as P
 from oracle.pyoracle import RefError
 from tests import refcases as RC
@@ -247,11 +248,11 @@ def test_host_encoder_matches_reference_goldens(native, name):
     codec = P.make_codec(name)
     page = RC.worked_page128()
     if name == "simdfastpfor":
-        e = P.encode_chunks(codec, page, np.array([0], np.uint64), np.array([128], np.uint32),
+        e = H.encode_chunks(codec, page, np.array([0], np.uint64), np.array([128], np.uint32),
                             raw=True)
         w = e.words[int(e.table["word_off"][0]):][:int(e.table["n_words"][0])]
         assert len(w) == 32 and int(w[0]) == 9 and int(w[9]) == 6
     if name == "simdbp128":
-        e = P.encode_chunks(codec, np.zeros(2048, np.uint32), np.array([0], np.uint64),
+        e = H.encode_chunks(codec, np.zeros(2048, np.uint32), np.array([0], np.uint64),
                             np.array([2048], np.uint32), raw=True)
         assert list(e.words[:int(e.table["n_words"][0])]) == [0, 0, 0, 0]

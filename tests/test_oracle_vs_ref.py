@@ -6,6 +6,7 @@ import zlib
 import numpy as np
 import pytest
 
+import harness as H
 import paper_1209_2137_b200 as P
 from oracle.pyoracle import RefError
 from tests.helpers import F3_NAMES, REF_NAMES, assorted_arrays, chunks_of, random_sorted
@@ -47,7 +48,7 @@ def test_encode_decode_match_reference(oracle, ref, name):
 def test_host_encoder_bit_exact(native, ref, name):
     codec = P.make_codec(name)
     for arr in assorted_arrays(seed=7 + zlib.crc32(name.encode()) % 991):
-        enc = P.encode_array(codec, arr)
+        enc = H.encode_array(codec, arr)
         mine = chunks_of(enc)
         theirs = ref.encode_array(name, arr)
         assert [n for n, _ in mine] == [n for n, _ in theirs]
@@ -64,7 +65,7 @@ def test_host_encoder_deltas_every_width(native, ref, codec_name):
         vals = (rng.integers(0, 2**32, size=n, dtype=np.uint64) & ((1 << b) - 1)).astype(np.uint32)
         if b % 3 == 0 and n > 128:  # outliers exercise FastPFOR exceptions
             vals[::37] = rng.integers(0, 2**32, size=len(vals[::37]), dtype=np.uint64)
-        e = P.encode_chunks(codec, vals, np.array([0], np.uint64), np.array([n], np.uint32),
+        e = H.encode_chunks(codec, vals, np.array([0], np.uint64), np.array([n], np.uint32),
                             raw=True)
         mine = e.words[int(e.table["word_off"][0]):][:int(e.table["n_words"][0])]
         assert np.array_equal(mine, ref.encode_deltas(codec_name, vals))
@@ -73,11 +74,11 @@ def test_host_encoder_deltas_every_width(native, ref, codec_name):
 def test_host_encoder_wrapping_matches_reference(native, ref):
     """sums wrap mod 2^32; the reference-side wrapping
     encoder (shim over Codec::encode_deltas) and ours agree."""
-    vals, _ = P.gen_arrays("geometric", 4, 65536, 32, seed=3, rate_ppm=100000)
+    vals, _ = H.gen_arrays("geometric", 4, 65536, 32, seed=3, rate_ppm=100000)
     for name in ("simdfastpfor-s4", "simdbp128-s4"):
         codec = P.make_codec(name)
         for row in vals:
-            e = P.encode_array(codec, row, allow_wrap=True)
+            e = H.encode_array(codec, row, allow_wrap=True)
             mine = chunks_of(e)[0][1]
             assert np.array_equal(mine, ref.encode_chunk_wrapping(name, row))
             assert np.array_equal(ref.decode_array(name, [(len(row), mine)]), row)

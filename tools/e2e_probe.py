@@ -2,14 +2,15 @@
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+import harness as H
 import paper_1209_2137_b200 as P
 count = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-vals, _ = P.gen_arrays("cluster", count, 65536, (20, 29), seed=1)
+vals, _ = H.gen_arrays("cluster", count, 65536, (20, 29), seed=1)
 flat = vals.reshape(-1)
 offs = np.arange(count, dtype=np.uint64) * 65536
 for name in ("simdbp128-s4", "simdfastpfor-s4"):
     codec = P.make_codec(name)
-    e = P.encode_chunks(codec, flat, offs, np.full(count, 65536, np.uint32))
+    e = H.encode_chunks(codec, flat, offs, np.full(count, 65536, np.uint32))
     hw = torch.empty(len(e.words), dtype=torch.int32, pin_memory=True)
     hw.numpy().view(np.uint32)[:] = e.words
     ho = torch.empty(e.n_out, dtype=torch.int32, pin_memory=True)

@@ -5,13 +5,14 @@ L2 flushed between repetitions."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+import harness as H
 import paper_1209_2137_b200 as P
 from oracle.pyoracle import Reference
 from paper_1209_2137_b200.device import host_checksum
 
 ref = Reference()
 count = int(os.environ.get("F3_ARRAYS", "1024"))
-vals, _ = P.gen_arrays("cluster", count, 65536, (20, 29), seed=1)
+vals, _ = H.gen_arrays("cluster", count, 65536, (20, 29), seed=1)
 flat = vals.reshape(-1)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for name in sys.argv[1:] or ["bp32-s4", "fastpfor-s4", "simplepfor-s4", "simdbp128-s4",

@@ -9,6 +9,7 @@ path.  CODEC=<name> picks the codec (default simdbp128-s4)."""
 import sys, os, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+import harness as H
 import paper_1209_2137_b200 as P
 
 na, nb = int(os.environ.get("NA", 1 << 26)), int(os.environ.get("NB", 1 << 22))
@@ -17,7 +18,7 @@ a = np.cumsum(rng.integers(1, 40, size=na, dtype=np.uint64)).astype(np.uint32)
 pick = rng.random(na) < (nb / na) * 0.5
 b = np.unique(np.concatenate([a[pick], np.cumsum(rng.integers(1, 40 * na // nb, size=nb // 2, dtype=np.uint64)).astype(np.uint32)])).astype(np.uint32)
 codec = P.make_codec(os.environ.get("CODEC", "simdbp128-s4"))
-ea, eb = P.encode_array(codec, a), P.encode_array(codec, b)
+ea, eb = H.encode_array(codec, a), H.encode_array(codec, b)
 want = np.intersect1d(a, b)
 def cpu_isect(a, b):  # sorted inputs: binary-search the shorter in the longer (the GPU's algorithm)
     s, l = (a, b) if len(a) <= len(b) else (b, a)

@@ -2,12 +2,13 @@
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+import harness as H
 import paper_1209_2137_b200 as P
 from oracle.pyoracle import Reference
 name = sys.argv[1]
 count = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
 ref = Reference()
-vals, _ = P.gen_arrays("cluster", count, 65536, (20, 29), seed=1)
+vals, _ = H.gen_arrays("cluster", count, 65536, (20, 29), seed=1)
 codec = P.make_codec(name)
 payloads, counts = [], []
 for row in vals:

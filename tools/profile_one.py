@@ -2,6 +2,7 @@
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+import harness as H
 import paper_1209_2137_b200 as P
 
 CFG = {
@@ -16,9 +17,9 @@ CFG = {
 name, model, count, d, rate, raw = CFG[sys.argv[1]]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 codec = P.make_codec(name)
-vals, _ = P.gen_arrays(model, count, 65536, d, seed=1, rate_ppm=rate)
+vals, _ = H.gen_arrays(model, count, 65536, d, seed=1, rate_ppm=rate)
 flat = vals.reshape(-1)
-enc = P.encode_chunks(codec, flat, np.arange(count, dtype=np.uint64) * 65536,
+enc = H.encode_chunks(codec, flat, np.arange(count, dtype=np.uint64) * 65536,
                       np.full(count, 65536, np.uint32), allow_wrap=model == "geometric", raw=raw)
 b = P.DeviceBatch(codec, enc, raw=raw)
 for _ in range(reps):

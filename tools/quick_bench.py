@@ -2,15 +2,16 @@
 import sys, os, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+import harness as H
 import paper_1209_2137_b200 as P
 
 def run(name, model, count, d, seed=1, rate=0, reps=20, raw=False):
     codec = P.make_codec(name)
     t0 = time.time()
-    vals, _ = P.gen_arrays(model, count, 65536, d, seed=seed, rate_ppm=rate)
+    vals, _ = H.gen_arrays(model, count, 65536, d, seed=seed, rate_ppm=rate)
     flat = vals.reshape(-1)
     offs = np.arange(count, dtype=np.uint64) * 65536
-    enc = P.encode_chunks(codec, flat, offs, np.full(count, 65536, np.uint32),
+    enc = H.encode_chunks(codec, flat, offs, np.full(count, 65536, np.uint32),
                           allow_wrap=(model == "geometric"), raw=raw)
     t1 = time.time()
     b = P.DeviceBatch(codec, enc, raw=raw, indexed=os.environ.get("IZG_FUSED") != "1")
@@ -56,7 +57,7 @@ def run_encode(name, model, count, d, rate=0, reps=10):
     """GPU encoder throughput (izg_encode) on device-resident values."""
     import paper_1209_2137_b200._native as N
     codec = P.make_codec(name)
-    vals, _ = P.gen_arrays(model, count, 65536, d, seed=3, rate_ppm=rate)
+    vals, _ = H.gen_arrays(model, count, 65536, d, seed=3, rate_ppm=rate)
     flat = vals.reshape(-1)
     L = N.lib()
     counts = np.full(count, 65536, np.uint32)

@@ -12,6 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 
+import harness as H
 import paper_1209_2137_b200 as P
 
 
@@ -32,9 +33,9 @@ for name, model, d, rate in [("simdbp128-s4", "cluster", 29, 0),
                              ("simdfastpfor-s4", "geometric", 32, 100000)]:
     codec = P.make_codec(name)
     for count in [64, 128, 256, 512, 1024, 2048, 4096]:
-        vals, _ = P.gen_arrays(model, count, 65536, d, seed=1, rate_ppm=rate)
+        vals, _ = H.gen_arrays(model, count, 65536, d, seed=1, rate_ppm=rate)
         flat = vals.reshape(-1)
-        enc = P.encode_chunks(codec, flat, np.arange(count, dtype=np.uint64) * 65536,
+        enc = H.encode_chunks(codec, flat, np.arange(count, dtype=np.uint64) * 65536,
                               np.full(count, 65536, np.uint32), allow_wrap=model == "geometric")
         ws = P.DeviceBatch(codec, enc)
         one = P.DeviceBatch(codec, enc, indexed=False, out=ws.out)

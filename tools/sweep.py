@@ -14,6 +14,7 @@ peak = MEASURED_PEAKS.json hbm_gbs when present, else 6532.9 GB/s.
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
+import harness as H
 import paper_1209_2137_b200 as P
 from paper_1209_2137_b200.device import host_checksum
 
@@ -43,9 +44,9 @@ def timed(b, reps=20):
 
 def run(name, model, count, d, raw, PK):
     codec = P.make_codec(name)
-    vals, _ = P.gen_arrays(model, count, 65536, d, seed=11)
+    vals, _ = H.gen_arrays(model, count, 65536, d, seed=11)
     flat = vals.reshape(-1)
-    enc = P.encode_chunks(codec, flat, np.arange(count, dtype=np.uint64) * 65536,
+    enc = H.encode_chunks(codec, flat, np.arange(count, dtype=np.uint64) * 65536,
                           np.full(count, 65536, np.uint32), raw=raw)
     b = P.DeviceBatch(codec, enc, raw=raw)
     t = timed(b)
