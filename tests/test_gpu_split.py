@@ -134,6 +134,7 @@ def test_split_corruption_statuses(cuda, name):
 _LARGE = r'''
 import sys
 sys.path.insert(0, {root!r})
+import harness as H
 import numpy as np, paper_1209_2137_b200 as P
 for name, model, d, rate, count in [("simdbp128-s4", "cluster", 29, 0, 2048),
                                     ("simdfastpfor-s4", "geometric", 32, 100000, 1024)]:
