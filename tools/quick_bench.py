@@ -48,6 +48,7 @@ if __name__ == "__main__":
         if w == "c4_1": run("simdfastpfor-s4", "geometric", 2048, 32, rate=10000)
         if w == "c5fp": run("simdfastpfor-s4", "cluster", 8192, (20, 29))
         if w == "c5bp": run("simdbp128-s4", "cluster", 8192, (20, 29))
+        if w == "c5fpbig": run("simdfastpfor-s4", "cluster", 32768, (20, 29), reps=8)
         if w == "fp29": run("simdfastpfor-s4", "cluster", 8192, 29)
         if w == "raw":
             for b in (0, 8, 16, 24, 32): run("simdbp128", "raw", 4096, b, raw=True)
