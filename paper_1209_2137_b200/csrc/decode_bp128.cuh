@@ -96,42 +96,6 @@ __device__ __forceinline__ void unpack_slots_aligned(const WarpRing& r, uint32_t
   }
 }
 
-// Lane-per-slot unpack of ONE vertical block straight into an output tile:
-// lane l extracts slot l of the block's four vertical lanes, i.e. integers
-// 4l .. 4l+3 of the block (bitpack.h:18-23), from row (l*w)/32 and — only
-// when the field straddles — the next, and stores them as one 16-byte word
-// at tile integer 128q + 4l (`dst` = TileSlot::at(q)).  The width is
-// warp-uniform here, so there is no per-lane sliding window: two loads, four
-// funnel shifts, four masks and one store per lane per block, against the
-// mapping-C unpack's window bookkeeping.  A block past the
-// end is unpacked at w = 0 (zeros), which keeps the prefix sum exact.
-__device__ __forceinline__ void unpack_block_tile(const WarpRing& r, uint32_t bb, uint32_t w,
-                                                  uint32_t dst, int lane) {
-  const uint32_t bit = (uint32_t)lane * w;
-  const uint32_t a = bb + ((bit >> 5) << 4), sh = bit & 31u;
-  const uint4 lo = lds128(r.base + (a & kRingMask));
-  uint4 hi = make_uint4(0u, 0u, 0u, 0u);
-  if (sh + w > 32u) hi = lds128(r.base + ((a + 16u) & kRingMask));
-  const uint32_t m = low_mask(w);
-  sts128(dst, funnel_r(lo.x, hi.x, sh) & m, funnel_r(lo.y, hi.y, sh) & m,
-         funnel_r(lo.z, hi.z, sh) & m, funnel_r(lo.w, hi.w, sh) & m);
-}
-
-// Swizzled tile address (OutStage::swz) of integers 128q + 4l .. +3 for
-// lane l: rows 4q + l/8 of the 128-byte-swizzled tile, 16-byte chunk l%8
-// XOR the row's low three bits, which only depend on q's parity.
-struct TileSlot {
-  uint32_t even, odd;  // byte offsets for q = 0 (q = 2: +1024) and q = 1 (q = 3: +1024)
-  __device__ __forceinline__ explicit TileSlot(int lane) {
-    const uint32_t rr = (uint32_t)lane >> 3, c = (uint32_t)lane & 7u;
-    even = (rr << 7) + ((c ^ rr) << 4);
-    odd = 512u + (rr << 7) + ((c ^ (rr + 4u)) << 4);
-  }
-  __device__ __forceinline__ uint32_t at(uint32_t t, uint32_t q) const {
-    return t + ((q >> 1) << 10) + ((q & 1u) ? odd : even);
-  }
-};
-
 // Same, two row loads per slot and no window: fewer instructions, more
 // shared-memory wavefronts.
 __device__ __forceinline__ void unpack_slots_rows(const WarpRing& r, uint32_t bb, uint32_t width,

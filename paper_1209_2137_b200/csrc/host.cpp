@@ -123,6 +123,7 @@ struct Slot {
   uint32_t* out = nullptr;
   uint64_t out_cap = 0;
   int32_t* status = nullptr;
+  uint64_t status_cap = 0;
   uint8_t* ws = nullptr;  // izg_decode_ws workspace (SIMD-FastPFOR index pass)
   uint64_t ws_cap = 0;
   cudaEvent_t decoded = nullptr;   // piece decoded: its D2H may start
@@ -235,11 +236,12 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     const long v = e ? std::atol(e) : 0;
     return (uint64_t)(v > 0 ? v : 16) << 20;
   }();
+  // (and at most 2^20 chunks, so batches of tiny chunks still pipeline)
   if (ordered) {
     uint64_t acc = 0;
     for (uint32_t i = 0; i < n_chunks; ++i) {
       acc += h_chunks[i].n;
-      if (acc >= piece_ints && i + 1 < n_chunks) {
+      if ((acc >= piece_ints || i + 1 - cuts.back() >= (1u << 20)) && i + 1 < n_chunks) {
         cuts.push_back(i + 1);
         acc = 0;
       }
@@ -262,6 +264,7 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
   std::memcpy(S.pin_table, h_chunks, sizeof(izg_chunk) * n_chunks);
   int32_t* st_host = S.pin_status;
   int rc = IZG_SUCCESS;
+  std::vector<std::pair<uint64_t, uint64_t>> runs;  // output ranges to copy back
   for (size_t p = 0; p + 1 < cuts.size() && rc == IZG_SUCCESS; ++p) {
     Slot& s = S.slot[p % kSlots];
     const uint32_t c0 = cuts[p], c1 = cuts[p + 1], nc = c1 - c0;
@@ -284,42 +287,63 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
       break;
     }
     s.table_cap = (uint32_t)tcap;
-    if (!s.status) {
-      if (cudaMalloc(&s.status, sizeof(int32_t) * (1u << 20)) != cudaSuccess) {
-        rc = IZG_ERR_CUDA;
-        break;
-      }
-    }
-    if (nc > (1u << 20)) {
-      rc = IZG_ERR_INVALID_ARGUMENT;
+    if (!grow(s.status, s.status_cap, nc)) {
+      rc = IZG_ERR_CUDA;
       break;
+    }
+    // The piece's table, rebased onto the slot's buffers (word wlo and
+    // output olo become offset 0).
+    for (uint32_t i = c0; i < c1; ++i) {
+      S.pin_table[i].word_off -= wlo;
+      S.pin_table[i].out_off -= olo;
     }
     for (auto& e : s.drained) cudaStreamWaitEvent(s.stream, e, 0);  // previous D2H done
     cudaMemsetAsync(s.words + wcopy, 0, (wneed - wcopy) * 4, s.stream);
     cudaMemcpyAsync(s.words, h_words + wlo, wcopy * 4, cudaMemcpyHostToDevice, s.stream);
     cudaMemcpyAsync(s.table, S.pin_table + c0, sizeof(izg_chunk) * nc, cudaMemcpyHostToDevice,
                     s.stream);
-    // Shifted base pointers: the kernel adds the table's absolute offsets.
-    const int r = izg_decode_ws(codec, delta, s.words - wlo, s.table, nc, s.out - olo,
-                                s.status, nullptr, s.ws, wsb, s.stream);
+    const int r = izg_decode_ws(codec, delta, s.words, s.table, nc, s.out, s.status, nullptr,
+                                s.ws, wsb, s.stream);
     if (r != IZG_SUCCESS) {
       rc = r;
       break;
     }
     cudaEventRecord(s.decoded, s.stream);
-    const uint64_t nout = ohi - olo, part = (nout / Scratch::kParts + 1023) & ~uint64_t{1023};
-    for (int k = 0; k < Scratch::kParts; ++k) {
-      cudaStreamWaitEvent(S.d2h[k], s.decoded, 0);
-      const uint64_t a = std::min<uint64_t>(nout, k * part);
-      const uint64_t b = k + 1 == Scratch::kParts ? nout : std::min<uint64_t>(nout, a + part);
-      if (b > a)
-        cudaMemcpyAsync(h_out + olo + a, s.out + a, (b - a) * 4, cudaMemcpyDeviceToHost,
-                        S.d2h[k]);
-      if (k == 0)
-        cudaMemcpyAsync(st_host + c0, s.status, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost,
-                        S.d2h[0]);
-      cudaEventRecord(s.drained[k], S.d2h[k]);
+    // Copy back only what the chunks decoded: the output ranges of the
+    // piece, merged where they touch.  Gaps between chunks in h_out keep the
+    // caller's contents (the device buffer holds no data for them).
+    runs.clear();
+    for (uint32_t i = c0; i < c1; ++i)
+      if (h_chunks[i].n) runs.push_back({h_chunks[i].out_off - olo, h_chunks[i].n});
+    if (!ordered) std::sort(runs.begin(), runs.end());
+    size_t m = 0;
+    for (size_t i = 0; i < runs.size(); ++i) {
+      if (m && runs[i].first <= runs[m - 1].first + runs[m - 1].second) {
+        const uint64_t e = std::max(runs[m - 1].first + runs[m - 1].second,
+                                    runs[i].first + runs[i].second);
+        runs[m - 1].second = e - runs[m - 1].first;
+      } else {
+        runs[m++] = runs[i];
+      }
     }
+    runs.resize(m);
+    if (runs.size() == 1) {  // contiguous: kParts concurrent copies keep D2H at ~56 GB/s
+      const uint64_t r0 = runs[0].first, nout = runs[0].second;
+      const uint64_t part = (nout / Scratch::kParts + 1023) & ~uint64_t{1023};
+      runs.clear();
+      for (int k = 0; k < Scratch::kParts; ++k) {
+        const uint64_t a = std::min<uint64_t>(nout, k * part);
+        const uint64_t b = k + 1 == Scratch::kParts ? nout : std::min<uint64_t>(nout, a + part);
+        if (b > a) runs.push_back({r0 + a, b - a});
+      }
+    }
+    for (int k = 0; k < Scratch::kParts; ++k) cudaStreamWaitEvent(S.d2h[k], s.decoded, 0);
+    for (size_t i = 0; i < runs.size(); ++i)
+      cudaMemcpyAsync(h_out + olo + runs[i].first, s.out + runs[i].first, runs[i].second * 4,
+                      cudaMemcpyDeviceToHost, S.d2h[i % Scratch::kParts]);
+    cudaMemcpyAsync(st_host + c0, s.status, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost,
+                    S.d2h[0]);
+    for (int k = 0; k < Scratch::kParts; ++k) cudaEventRecord(s.drained[k], S.d2h[k]);
   }
   for (auto& s : S.slot)
     if (cudaStreamSynchronize(s.stream) != cudaSuccess) rc = IZG_ERR_CUDA;

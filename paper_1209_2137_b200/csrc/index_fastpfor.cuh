@@ -28,10 +28,6 @@
 #include "decode_fastpfor.cuh"
 #include "izg_common.cuh"
 
-#ifndef IZG_TILE_UNPACK
-#define IZG_TILE_UNPACK 1  // lane-per-slot block unpack into the tile
-#endif
-
 namespace izg {
 
 constexpr uint32_t kMaxBlocks = IZG_CHUNK_SIZE / 128;  // 512 records per page
@@ -211,9 +207,6 @@ __device__ bool fp_blocks_idx(WarpRing& r, OS& os, const uint32_t* dir_base, con
   const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
   bool bad = false;
   uint4 nx = rec[min(q, nblocks - 1)];
-#if IZG_TILE_UNPACK
-  const TileSlot slot(lane);
-#endif
 #pragma unroll 1
   for (uint32_t g0 = 0; g0 < nblocks; g0 += 4) {
     const uint32_t ng = min(4u, nblocks - g0);
@@ -236,36 +229,6 @@ __device__ bool fp_blocks_idx(WarpRing& r, OS& os, const uint32_t* dir_base, con
     r.release_below(4u * (first - wbase));
     r.ensure(4u * (after - wbase));
     uint32_t v[4][4];
-#if IZG_TILE_UNPACK
-    if (ST == kVertical && r.phase == 0) {
-      // the four blocks unpack lane-per-slot into the tile (warp-uniform
-      // width per block), get patched there, and are read back in mapping C
-      const uint32_t t = os.acquire();
-      const uint32_t roff = r.ring_off();
-#pragma unroll
-      for (uint32_t k = 0; k < 4; ++k) {
-        const uint32_t bk = __shfl_sync(0xFFFFFFFFu, myb, 8 * k);
-        const uint32_t ok = __shfl_sync(0xFFFFFFFFu, myoff, 8 * k);
-        unpack_block_tile(r, roff + 4u * (ok - wbase), bk, slot.at(t, k), lane);
-      }
-      __syncwarp();
-      if (tot) {
-#ifndef IZG_ABL_NOPATCH
-        bad |= fp_patch<ST>(t, page, ba, myb, myw, myc, mybp, mycur, dir_base[myw], lane);
-#endif
-        __syncwarp();
-      }
-      OutStage::read(t, v, lane);
-      scan<DELTA>(v, carry, lane);
-      if (orow >= 0 && ng == 4) {
-        os.commit(v, lane, (uint32_t)(orow + 4 * g0));
-      } else {
-        os.abandon();
-        os.direct(v, out + (size_t)(g0 + q) * 128 + 16 * s8, oal, live, 128u * ng, lane);
-      }
-      continue;
-    }
-#endif
     if (ST != kVertical)
       unpack_scalar_slots(r, myoff - wbase, myb, s8, v);
     else if (r.phase == 0)

@@ -211,3 +211,52 @@ def test_bp128_warps_per_chunk(kw):
     r = subprocess.run([sys.executable, "-c", _GROUP.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+def test_host_decode_many_tiny_chunks(cuda, ref):
+    """izg_decode_host with more than 2^20 chunks (1-integer arrays, as short
+    posting lists give): the reference's decode_array accepts any number of
+    chunks, so must the host path (it cuts pieces by chunk count too)."""
+    codec = P.make_codec("simdbp128-s4")
+    n = (1 << 20) + 4097
+    vals = np.random.default_rng(8).integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+    enc = H.encode_chunks(codec, vals, np.arange(n, dtype=np.uint64), np.ones(n, np.uint32))
+    got = P.decode_array(codec, enc)
+    assert np.array_equal(got, vals)
+    # spot-check the payload words against the reference encoder
+    for i in (0, n // 2, n - 1):
+        chunks = ref.encode_array("simdbp128-s4", vals[i:i + 1])
+        t = enc.table[i]
+        assert np.array_equal(chunks[0][1], enc.words[int(t["word_off"]):][:int(t["n_words"])])
+
+
+def test_host_decode_leaves_gaps_untouched(cuda):
+    """Outputs placed with gaps between chunks: izg_decode_host copies back
+    only the decoded ranges, the caller's other words stay as they were."""
+    import ctypes as C  # noqa: F401
+
+    codec = P.make_codec("simdfastpfor-s4")
+    rng = np.random.default_rng(12)
+    arrs = [random_sorted(rng, n, 1000) for n in (70000, 300, 4096 + 5, 65536)]
+    encs = [H.encode_array(codec, a) for a in arrs]
+    payloads, counts, outs = [], [], []
+    pos = 7
+    for e in encs:
+        for t in e.table:
+            payloads.append(e.words[int(t["word_off"]):int(t["word_off"]) + int(t["n_words"])])
+            counts.append(int(t["n"]))
+            outs.append(pos)
+            pos += int(t["n"]) + 1000  # a gap after every chunk
+    enc = P.layout(codec, payloads, counts, np.array(outs, dtype=np.uint64))
+    L = P._native.lib()
+    out = np.full(pos, 0xA5A5A5A5, dtype=np.uint32)
+    st = np.zeros(len(counts), np.int32)
+    rc = L.izg_decode_host(codec.codec, codec.delta, P._native.ptr(enc.words), len(enc.words),
+                           P._native.ptr(enc.table), len(enc.table), P._native.ptr(out), len(out),
+                           P._native.ptr(st))
+    assert rc == 0 and not st.any()
+    mask = np.zeros(pos, bool)
+    for o, n in zip(outs, counts):
+        mask[o:o + n] = True
+    assert np.all(out[~mask] == 0xA5A5A5A5)
+    assert np.array_equal(out[mask], np.concatenate(arrs))
