@@ -22,7 +22,7 @@ LIB = os.path.join(LIBDIR, "libintzip_b200.so")
 OBJDIR = os.path.join(LIBDIR, "obj")
 
 SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "decode_split.cu",
-           "decode_group.cu", "intersect.cu", "host.cpp", "container.cpp"]
+           "decode_group.cu", "decode_cta.cu", "intersect.cu", "host.cpp", "container.cpp"]
 # per-source extra flags: see the comment at the top of decode_scalar.cu
 SOURCE_FLAGS = {"decode_scalar.cu": ["-Xptxas", "-O1"]}
 if os.environ.get("IZG_SCALAR_O1", "1") == "0":  # sanitizer repro builds only

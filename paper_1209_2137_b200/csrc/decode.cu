@@ -93,6 +93,30 @@ SplitFn pick_split(int codec, int delta);
 using GroupFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
                          uint32_t*, uint32_t*, const CUtensorMap, int);
 GroupFn pick_group(int kw, int delta);
+// CTA-cooperative SIMD-BP128 kernels (one CTA per SM): decode_cta.cu.
+GroupFn pick_cta(int delta);
+size_t cta_smem_bytes();
+int cta_threads();
+
+// SIMD-BP128 array-mode batches in [kCtaMinChunks, kCtaMaxChunks] take the
+// CTA-cooperative kernel (cta.cuh): with fewer chunks than ~2 per resident
+// warp, one warp per chunk is latency-bound.  IZG_CTA=0 / 1 forces it off /
+// on (tests, sweeps).
+#ifndef IZG_CTA_MIN
+#define IZG_CTA_MIN 256
+#endif
+#ifndef IZG_CTA_MAX
+#define IZG_CTA_MAX 8192
+#endif
+bool cta_wanted(int codec, int delta, uint32_t n_chunks) {
+  if (codec != IZG_SIMDBP128 || delta == IZG_DELTA_NONE) return false;
+  static const int force = [] {
+    const char* e = std::getenv("IZG_CTA");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (force >= 0) return force != 0;
+  return n_chunks >= IZG_CTA_MIN && n_chunks <= IZG_CTA_MAX;
+}
 
 // Warps per chunk for a SIMD-BP128 batch that does not take the split
 // kernel, by batch size against the resident warp slots.  IZG_GROUP=1, 2, 4
@@ -159,7 +183,7 @@ struct DeviceInfo {
   int sms = 0;
   // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink,
   //  + 3 kCodecs: split kernels, 4 kCodecs + 0..2: group kernels KW = 2, 4, 8)][delta]
-  int occ[4 * kCodecs + 4][5] = {};
+  int occ[4 * kCodecs + 5][5] = {};  // + 4 kCodecs + 3: big indexed, + 4: CTA kernel
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -298,6 +322,24 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                    delta, kfn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;
+  if (!probe && !split && cta_wanted(codec, delta, n_chunks)) {
+    GroupFn cfn = pick_cta(delta);
+    int cper_sm = 0, csms = 0;
+    uint32_t* ccounter = nullptr;
+    rc = prepare(dev, 4 * kCodecs + 4, delta, reinterpret_cast<const void*>(cfn), cta_threads(),
+                 cta_smem_bytes(), &cper_sm, &csms, &ccounter);
+    if (rc != IZG_SUCCESS) return rc;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(ccounter, 0, sizeof(uint32_t), cs) != cudaSuccess) return IZG_ERR_CUDA;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(n_chunks, (uint64_t)csms);
+    CUtensorMap omap;
+    std::memset(&omap, 0, sizeof(omap));
+    const int tma_out = IZG_TMA_STORE && make_out_map(&omap, d_out) ? 1 : 0;
+    cfn<<<grid, cta_threads(), cta_smem_bytes(), cs>>>(d_words, d_chunks, n_chunks, d_out,
+                                                       d_status, d_consumed, ccounter, omap,
+                                                       tma_out);
+    return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+  }
   if (codec == IZG_SIMDBP128 && !probe && !split) {
     // SIMD-BP128 small batches: KW warps per chunk (group.cuh); the one-warp
     // kernel's warp slots (same registers and ring) set KW

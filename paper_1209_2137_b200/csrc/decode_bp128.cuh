@@ -24,8 +24,8 @@ struct MetaWalk {
 // One meta-block descriptor at payload word `pos` with `groups` present
 // groups (codec_binpack.cpp:104-117): for each present group in order, a
 // width byte > 32 is an error, then a payload running past `nw` words.
-template <bool ALIGNED>
-__device__ __forceinline__ MetaWalk walk_meta(const WarpRing& r, uint32_t pos, uint32_t groups,
+template <bool ALIGNED, typename R>
+__device__ __forceinline__ MetaWalk walk_meta(const R& r, uint32_t pos, uint32_t groups,
                                               uint32_t nw, int lane) {
   uint32_t d0, d1, d2, d3;
   if (ALIGNED) {
@@ -68,15 +68,15 @@ __device__ __forceinline__ MetaWalk walk_meta(const WarpRing& r, uint32_t pos, u
 // unmasked ring byte `bb`, sliding a two-row window (lo, hi) down the block:
 // a 16-byte row is fetched only when the bit cursor enters it, so each lane
 // reads each row it needs once (bitpack.cpp:122-143 restated per lane).
-__device__ __forceinline__ void unpack_slots_aligned(const WarpRing& r, uint32_t bb,
-                                                     uint32_t width, uint32_t s8,
-                                                     uint32_t (&v)[4][4]) {
+template <typename R>
+__device__ __forceinline__ void unpack_slots_aligned(const R& r, uint32_t bb, uint32_t width,
+                                                     uint32_t s8, uint32_t (&v)[4][4]) {
   const uint32_t mask = low_mask(width);
   uint32_t bit = 4u * s8 * width;
   uint32_t row = bit >> 5;
   uint32_t ra = bb + 16u * row;
-  uint4 lo = lds128(r.base + (ra & kRingMask));
-  uint4 hi = lds128(r.base + ((ra + 16u) & kRingMask));
+  uint4 lo = lds128(r.base + (ra & R::kMask));
+  uint4 hi = lds128(r.base + ((ra + 16u) & R::kMask));
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     if (c) {
@@ -85,7 +85,7 @@ __device__ __forceinline__ void unpack_slots_aligned(const WarpRing& r, uint32_t
         ++row;
         ra += 16u;
         lo = hi;
-        hi = lds128(r.base + ((ra + 16u) & kRingMask));
+        hi = lds128(r.base + ((ra + 16u) & R::kMask));
       }
     }
     const uint32_t sh = bit & 31u;
@@ -115,7 +115,8 @@ __device__ __forceinline__ void unpack_slots_rows(const WarpRing& r, uint32_t bb
 }
 
 // Same for a payload that is not 16-byte aligned in the ring: word loads.
-__device__ __forceinline__ void unpack_slots_unaligned(const WarpRing& r, uint32_t bword,
+template <typename R>
+__device__ __forceinline__ void unpack_slots_unaligned(const R& r, uint32_t bword,
                                                        uint32_t width, uint32_t s8,
                                                        uint32_t (&v)[4][4]) {
   const uint32_t mask = low_mask(width);

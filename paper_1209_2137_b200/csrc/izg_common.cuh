@@ -96,6 +96,7 @@ struct Layout {
 // issues the copies.  Chunk payloads stream as the 16-byte-aligned span
 // covering them; `phase` is payload word 0's byte offset in that span.
 struct WarpRing {
+  static constexpr uint32_t kMask = kRingMask;
   uint32_t base;        // shared address of the ring
   uint32_t bar;         // shared address of its kNS mbarriers (8 bytes each)
   uint32_t g;           // stages consumed before the current chunk
