@@ -19,6 +19,26 @@ GroupFn pick_cta(int delta) {
 }
 
 size_t cta_smem_bytes() { return CtaLayout::kSmem; }
+
+}  // namespace izg
+
+#ifdef IZG_CTA_PROF
+extern "C" int izg_debug_cta_trace(void* host) {
+  return cudaMemcpyFromSymbol(host, izg::g_cta_trace, sizeof(izg::g_cta_trace)) == cudaSuccess ? 0 : -1;
+}
+extern "C" int izg_debug_cta_prof(void* host, size_t bytes, int reset) {
+  if (bytes > sizeof(izg::g_cta_prof)) bytes = sizeof(izg::g_cta_prof);
+  if (cudaMemcpyFromSymbol(host, izg::g_cta_prof, bytes) != cudaSuccess) return -1;
+  if (reset) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, izg::g_cta_prof) != cudaSuccess) return -1;
+    cudaMemset(p, 0, sizeof(izg::g_cta_prof));
+  }
+  return 0;
+}
+#endif
+
+namespace izg {
 int cta_threads() { return kCtaWarps * 32; }
 
 }  // namespace izg
