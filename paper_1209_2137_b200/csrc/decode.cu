@@ -98,15 +98,20 @@ GroupFn pick_cta(int delta);
 size_t cta_smem_bytes();
 int cta_threads();
 
-// SIMD-BP128 array-mode batches in [kCtaMinChunks, kCtaMaxChunks] take the
+// SIMD-BP128 array-mode batches of up to IZG_CTA_MAX chunks take the
 // CTA-cooperative kernel (cta.cuh): with fewer chunks than ~2 per resident
-// warp, one warp per chunk is latency-bound.  IZG_CTA=0 / 1 forces it off /
-// on (tests, sweeps).
+// warp, one warp per chunk is latency-bound.  Measured on B200
+// (tools/cta_sweep.py, 65,536-integer ClusterData d=29 chunks, ms, CTA vs
+// the path taken otherwise): 64: 0.025 vs 0.041 (split); 128: 0.025 vs
+// 0.047; 256: 0.037 vs 0.074; 384: 0.049 vs 0.083; 512: 0.061 vs 0.090
+// (group KW 4); 768: 0.086 vs 0.110; 1,024 (C1): 0.102 vs 0.115 (one warp
+// per chunk); 1,536: 0.148 vs 0.151; 2,048: 0.190 vs 0.151.  IZG_CTA=0 / 1
+// forces it off / on (tests, sweeps).
 #ifndef IZG_CTA_MIN
-#define IZG_CTA_MIN 256
+#define IZG_CTA_MIN 1
 #endif
 #ifndef IZG_CTA_MAX
-#define IZG_CTA_MAX 8192
+#define IZG_CTA_MAX 1600
 #endif
 bool cta_wanted(int codec, int delta, uint32_t n_chunks) {
   if (codec != IZG_SIMDBP128 || delta == IZG_DELTA_NONE) return false;
@@ -322,7 +327,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                    delta, kfn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;
-  if (!probe && !split && cta_wanted(codec, delta, n_chunks)) {
+  if (!probe && cta_wanted(codec, delta, n_chunks)) {
     GroupFn cfn = pick_cta(delta);
     int cper_sm = 0, csms = 0;
     uint32_t* ccounter = nullptr;
