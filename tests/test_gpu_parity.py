@@ -207,7 +207,7 @@ def test_bp128_warps_per_chunk(kw):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, IZG_GROUP=str(kw), IZG_SPLIT="0")
+    env = dict(os.environ, IZG_GROUP=str(kw), IZG_SPLIT="0", IZG_CTA="0")
     r = subprocess.run([sys.executable, "-c", _GROUP.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]

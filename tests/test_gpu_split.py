@@ -3,7 +3,10 @@ carry) against the one-warp-per-chunk kernel and the original arrays.
 
 Small batches take the split kernel whenever a workspace is given
 (DeviceBatch(indexed=True)); DeviceBatch(indexed=False) runs izg_decode, the
-one-warp kernel, which the parity suites pin to the reference.  Outputs must
+one-warp kernel, which the parity suites pin to the reference.  Small
+SIMD-BP128 array batches now default to the CTA kernel (csrc/cta.cuh) on
+both sides, so the SIMD-BP128 split paths are exercised in subprocesses with
+IZG_CTA=0 (test_split_large_batch_forced, test_split_segment_sizes).  Outputs must
 match word for word and statuses exactly, including under corruption (the
 first error of a chunk in stream order travels with the look-back)."""
 import numpy as np
@@ -162,7 +165,7 @@ def test_split_large_batch_forced():
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, IZG_SPLIT="1")
+    env = dict(os.environ, IZG_SPLIT="1", IZG_CTA="0")
     r = subprocess.run([sys.executable, "-c", _LARGE.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
@@ -193,7 +196,7 @@ def test_split_segment_sizes(segs):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, IZG_SPLIT_SEGS=str(segs))
+    env = dict(os.environ, IZG_SPLIT_SEGS=str(segs), IZG_CTA="0")
     r = subprocess.run([sys.executable, "-c", _SEGS.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
