@@ -305,6 +305,7 @@ static __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint
                                 int lane, uint32_t* end) {
   sc.dir_n[lane + 1] = 0;
   sc.dir_base[lane + 1] = 0;
+  if (lane == 0) sc.dir_base[0] = 0;  // width 0 (no exceptions): the page start
   __syncwarp();
   if (pos >= nw) return IZG_E_FP_NO_BITSET;
   uint32_t bits = ldg_u32(page + pos);
@@ -345,10 +346,68 @@ static __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint
 #ifndef IZG_PATCH_SLOTS
 #define IZG_PATCH_SLOTS 2  // exceptions per lane per round (8 lanes per block)
 #endif
+// Vertical arrays (SIMD-FastPFOR): every address is formed from a valid
+// base, so no slot needs a select on its addresses — an idle slot (e >= c)
+// re-reads the block's exception 0, and a block without exceptions reads
+// width 0's base, which callers set to 0 (dir_base[0] = 0) — and the tile
+// address of position p in block q is built from per-lane constants (the
+// 128-byte swizzle's row parity depends only on q and p >> 5).
+#ifndef IZG_PATCH_LEAN
+#define IZG_PATCH_LEAN 1
+#endif
+__device__ __forceinline__ bool fp_patch_vertical(uint32_t t, const uint32_t* page,
+                                                  const uint8_t* ba, uint32_t myb, uint32_t myw,
+                                                  uint32_t myc, uint32_t mybp, uint32_t mycur,
+                                                  uint32_t mybase, int lane) {
+  const uint32_t q = (lane >> 3) & 3u, s8 = lane & 7;
+  uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));
+  mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));
+  const uint32_t wmask = low_mask(myw), w4 = 4u * myw;
+  const uint32_t* arr = page + mybase;
+  const uint8_t* pb = ba + mybp;
+  const uint32_t tq = t + (q << 9), rq = (q & 1u) << 2;
+  bool bad = false;
+  for (uint32_t e0 = s8; e0 < mxc; e0 += 8 * IZG_PATCH_SLOTS) {
+    uint32_t pp[IZG_PATCH_SLOTS], lo[IZG_PATCH_SLOTS], hi[IZG_PATCH_SLOTS], sh[IZG_PATCH_SLOTS];
+    bool ok[IZG_PATCH_SLOTS];
+#pragma unroll
+    for (int j = 0; j < IZG_PATCH_SLOTS; ++j) {
+      const uint32_t e = e0 + 8u * j;
+      ok[j] = e < myc;
+      const uint32_t rr = mycur + (ok[j] ? e : 0u);
+      const uint32_t tt = rr & 127u, bit = (tt >> 2) * myw;
+      const uint32_t word = (rr >> 7) * w4 + 4u * (bit >> 5) + (tt & 3u);
+      sh[j] = bit & 31u;
+      pp[j] = ok[j] ? ld_u8(pb + e) : 0u;
+      lo[j] = ld_u32(arr + word);
+      hi[j] = ld_u32(arr + word + (sh[j] + myw > 32 ? 4u : 0u));
+    }
+#pragma unroll
+    for (int j = 0; j < IZG_PATCH_SLOTS; ++j) {
+      if (ok[j]) {
+        const uint32_t p = pp[j];
+        if (p < 128u) {
+          const uint32_t hv = (funnel_r(lo[j], hi[j], sh[j]) & wmask) << myb;
+          const uint32_t r = p >> 5;
+          const uint32_t a = tq + (r << 7) + (((((p >> 2) & 7u) ^ (rq + r))) << 4) + ((p & 3u) << 2);
+          asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(hv));
+        } else {
+          bad = true;
+        }
+      }
+    }
+  }
+  return bad;
+}
+
 template <int ST>
 __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const uint8_t* ba,
                                          uint32_t myb, uint32_t myw, uint32_t myc, uint32_t mybp,
                                          uint32_t mycur, uint32_t mybase, int lane) {
+#if IZG_PATCH_LEAN
+  if constexpr (ST == kVertical)
+    return fp_patch_vertical(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
+#endif
   const uint32_t q = (lane >> 3) & 3u, s8 = lane & 7;
   uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));
   mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));

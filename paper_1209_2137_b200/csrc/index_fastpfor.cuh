@@ -291,6 +291,7 @@ __device__ int32_t fastpfor_core_idx(WarpRing& r, OS& os, uint32_t* dir_base,
   }
   const uint32_t A = h.w;
   dir_base[lane + 1] = ix.dir[(size_t)c * 32 + lane];
+  if (lane == 0) dir_base[0] = 0;  // width 0 (no exceptions): the page start
   __syncwarp();
   if (lane == 0) prefetch_l2(page + h.y, 4u * (h.z - h.y));  // exception arrays
   r.begin(page + 1, A - 1);

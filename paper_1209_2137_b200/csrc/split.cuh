@@ -484,6 +484,7 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
       } else {
         const uint4* rec = ix.page_rec(c);
         dir_base[lane + 1] = ix.dir[(size_t)c * 32 + lane];
+        if (lane == 0) dir_base[0] = 0;  // width 0 (no exceptions): the page start
         __syncwarp();
         const uint32_t A = hdr.w;
         const uint32_t wfirst = rec[b0].y;  // first packed word of the segment
