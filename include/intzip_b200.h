@@ -201,6 +201,20 @@ int izg_decode_ws(int codec, int delta, const uint32_t* d_words,
                   int32_t* d_status, uint32_t* d_consumed, void* d_workspace,
                   uint64_t workspace_bytes, void* stream);
 
+/* izg_decode_ws in two stream-ordered halves, so the SIMD-FastPFOR page
+ * index pass can run on another stream while other work runs (e.g. a
+ * SIMD-BP128 decode of the same step):
+ *   phase 1: the page index pass alone (fills the workspace);
+ *   phase 2: the decode alone, from a workspace phase 1 filled for the same
+ *            words and table (order the two with events/streams);
+ *   phase 0: both (= izg_decode_ws).
+ * On batches and codecs without the two-launch indexed path, phase 1 does
+ * nothing and phase 2 is the whole decode.  Results equal izg_decode_ws's. */
+int izg_decode_ws_phase(int codec, int delta, const uint32_t* d_words,
+                        const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
+                        int32_t* d_status, uint32_t* d_consumed, void* d_workspace,
+                        uint64_t workspace_bytes, int phase, void* stream);
+
 /* Order-sensitive checksum of n words: sum over i of (w_i + 1) * (2i + 1)
  * mod 2^64 (xor of all words in d_result[1]).  Used for whole-box parity with
  * an NCCL reduction; not part of the reference. */

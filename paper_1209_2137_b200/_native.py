@@ -60,6 +60,9 @@ def lib() -> C.CDLL:
     L.izg_decode_ws.restype = C.c_int
     L.izg_decode_ws.argtypes = [C.c_int, C.c_int, vp, vp, C.c_uint32, vp, vp, vp, vp,
                                 C.c_uint64, vp]
+    L.izg_decode_ws_phase.restype = C.c_int
+    L.izg_decode_ws_phase.argtypes = [C.c_int, C.c_int, vp, vp, C.c_uint32, vp, vp, vp, vp,
+                                      C.c_uint64, C.c_int, vp]
     L.izg_decode_workspace_size.restype = C.c_uint64
     L.izg_decode_workspace_size.argtypes = [C.c_int, C.c_uint32]
     L.izg_decode_index_workspace_size.restype = C.c_uint64
@@ -97,7 +100,7 @@ def lib() -> C.CDLL:
 
 # Symbols include/intzip_b200.h declares (checked by the CPU test suite).
 ABI_SYMBOLS = ("izg_status_string", "izg_parse_codec_name", "izg_layout_chunks",
-               "izg_decode", "izg_decode_ws", "izg_decode_workspace_size",
+               "izg_decode", "izg_decode_ws", "izg_decode_ws_phase", "izg_decode_workspace_size",
                "izg_decode_index_workspace_size", "izg_checksum", "izg_decode_host", "izg_release_host_scratch",
                "izg_encode", "izg_encode_bound", "izg_container_scan", "izg_container_index",
                "izg_container_decode_host", "izg_intersect_workspace_size",

@@ -262,9 +262,13 @@ namespace izg {
 
 // `probe` non-null: decode -> intersect (ProbeStage sink, no output; d_out
 // is unused and the indexed path is not taken).
+// `phase` (SIMD-FastPFOR's indexed path only): 0 = index pass + decode,
+// 1 = the page index pass alone, 2 = the decode alone from a workspace that
+// phase 1 filled for the same words and table (stream order).
 int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* d_chunks,
                 uint32_t n_chunks, uint32_t* d_out, int32_t* d_status, uint32_t* d_consumed,
-                void* d_ws, uint64_t ws_bytes, void* stream, const ProbeArgs* probe = nullptr) {
+                void* d_ws, uint64_t ws_bytes, void* stream, const ProbeArgs* probe = nullptr,
+                int phase = 0) {
   if (codec < IZG_SIMDBP128 || codec > IZG_SIMPLEPFOR) return IZG_ERR_INVALID_ARGUMENT;
   if (delta < IZG_DELTA_NONE || delta > IZG_DELTA_DM) return IZG_ERR_INVALID_ARGUMENT;
   if (probe && delta != IZG_DELTA_D1 && delta != IZG_DELTA_D4) return IZG_ERR_INVALID_ARGUMENT;
@@ -322,6 +326,10 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                      ws_bytes >= workspace_bytes(codec, n_chunks);
   const void* kfn = split ? reinterpret_cast<const void*>(pick_split(codec, delta))
                           : reinterpret_cast<const void*>(fn);
+  // phases only exist where a page index pass runs (the indexed decode and
+  // SIMD-FastPFOR's split decode): elsewhere phase 1 has nothing to do and
+  // phase 2 is the whole decode
+  if (phase == 1 && !idx) return IZG_SUCCESS;
   int rc = prepare(dev, big ? 4 * kCodecs + 3
                            : codec + (split ? 3 * kCodecs : idx ? kCodecs : probe ? 2 * kCodecs : 0),
                    delta, kfn, warps * 32, smem, &per_sm, &sms,
@@ -373,7 +381,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   IdxView ix{};
-  if (idx) {
+  if (idx && phase != 2) {
     static const bool attr = [] {
       const int b = (int)IdxLayout::kSmem;
       cudaFuncSetAttribute(fp_index_kernel<false, kVertical>,
@@ -388,6 +396,9 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     auto* ifn = delta == IZG_DELTA_NONE ? fp_index_kernel<false, kVertical>
                                         : fp_index_kernel<true, kVertical>;
     ifn<<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks, n_chunks, ix);
+    if (phase == 1) return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+  } else if (idx) {
+    ix = idx_view(d_ws, n_chunks);
   }
   if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
   if (split) {
@@ -416,7 +427,13 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
   }
   const uint64_t want = (n_chunks + warps - 1) / warps;
-  const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)per_sm * sms);
+  static const int cap_ctas = [] {  // IZG_BP_MAX_CTAS: co-residency experiments (SIMD-BP128)
+    const char* e = std::getenv("IZG_BP_MAX_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int eff_per_sm =
+      cap_ctas > 0 && codec == IZG_SIMDBP128 ? std::min(per_sm, cap_ctas) : per_sm;
+  const uint32_t grid = (uint32_t)std::min<uint64_t>(want, (uint64_t)eff_per_sm * sms);
   CUtensorMap omap;
   std::memset(&omap, 0, sizeof(omap));
   const int tma_out = !probe && IZG_TMA_STORE && make_out_map(&omap, d_out) ? 1 : 0;
@@ -485,6 +502,15 @@ extern "C" int izg_decode_ws(int codec, int delta, const uint32_t* d_words,
                              uint64_t workspace_bytes, void* stream) {
   return izg::decode_impl(codec, delta, d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
                           d_workspace, workspace_bytes, stream);
+}
+
+extern "C" int izg_decode_ws_phase(int codec, int delta, const uint32_t* d_words,
+                                   const izg_chunk* d_chunks, uint32_t n_chunks, uint32_t* d_out,
+                                   int32_t* d_status, uint32_t* d_consumed, void* d_workspace,
+                                   uint64_t workspace_bytes, int phase, void* stream) {
+  if (phase < 0 || phase > 2) return IZG_ERR_INVALID_ARGUMENT;
+  return izg::decode_impl(codec, delta, d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
+                          d_workspace, workspace_bytes, stream, nullptr, phase);
 }
 
 extern "C" int izg_checksum(const uint32_t* d_data, uint64_t n, uint64_t* d_result,

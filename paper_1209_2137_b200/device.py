@@ -81,6 +81,20 @@ class DeviceBatch:
         if rc != N.SUCCESS:
             raise RuntimeError(f"izg_decode failed: {rc}")
 
+    def decode_phase(self, phase: int, stream=None) -> None:
+        """izg_decode_ws_phase: 1 = the page index pass alone, 2 = the decode
+        alone (after phase 1 on the same batch, stream-ordered), 0 = both."""
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        ws = self.workspace
+        rc = N.lib().izg_decode_ws_phase(self.codec.codec, self.delta, N.ptr(self.words),
+                                         N.ptr(self.table), self.n_chunks, N.ptr(self.out),
+                                         N.ptr(self.status), N.ptr(self.consumed),
+                                         N.ptr(ws) if ws is not None else None,
+                                         ws.numel() if ws is not None else 0, phase,
+                                         s.cuda_stream)
+        if rc != N.SUCCESS:
+            raise RuntimeError(f"izg_decode_ws_phase failed: {rc}")
+
     def checksum(self, stream=None) -> tuple[int, int]:
         s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
         rc = N.lib().izg_checksum(N.ptr(self.out), self.n_out, N.ptr(self.sums), s.cuda_stream)
