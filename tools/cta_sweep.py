@@ -8,9 +8,10 @@ import harness as H
 import paper_1209_2137_b200 as P
 
 codec = P.make_codec(sys.argv[1] if len(sys.argv) > 1 else "simdbp128-s4")
-vals, _ = H.gen_arrays("cluster", 4096, 65536, 29, seed=1)
+counts = [int(x) for x in os.environ.get("COUNTS", "64,128,256,384,512,768,1024,1536,2048,3072,4096").split(",")]
+vals, _ = H.gen_arrays("cluster", max(counts), 65536, 29, seed=1)
 flat = vals.reshape(-1)
-for count in (64, 128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096):
+for count in counts:
     enc = H.encode_chunks(codec, flat[:count * 65536], np.arange(count, dtype=np.uint64) * 65536,
                           np.full(count, 65536, np.uint32))
     b = P.DeviceBatch(codec, enc)
@@ -26,5 +27,5 @@ for count in (64, 128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096):
         e0.record(); b.decode(); e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ok = np.array_equal(b.output()[:65536 * 2], flat[:65536 * 2])
-    print(json.dumps({"cta": os.environ.get("IZG_CTA"), "chunks": count, "ms": round(float(np.median(ts)), 4),
+    print(json.dumps({"cta": os.environ.get("IZG_CTA"), "tail": os.environ.get("IZG_CTA_TAIL"), "chunks": count, "ms": round(float(np.median(ts)), 4),
                       "ok": bool(ok)}), flush=True)
