@@ -228,14 +228,21 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     if (i && (c.word_off < h_chunks[i - 1].word_off || c.out_off < h_chunks[i - 1].out_off))
       ordered = false;
   }
-  // Pieces of about 64 MiB of output (enough chunks per launch to fill the
-  // GPU, small enough to keep both copy engines busy).
+  // Pieces of 16..64 Mi integers of output, about an eighth of the batch
+  // (enough chunks per launch to fill the GPU, enough pieces to overlap the
+  // H2D, decode and D2H stages; B200 + PCIe Gen5, 2^30-integer batches:
+  // 16 Mi pieces 51.0 GB/s D2H, 64 Mi 52.3, against 52.4 for one bare copy).
   std::vector<uint32_t> cuts{0};
-  static const uint64_t piece_ints = [] {
+  static const uint64_t forced_piece = [] {
     const char* e = std::getenv("IZG_HOST_PIECE_MI");  // tuning knob (integers, in Mi)
     const long v = e ? std::atol(e) : 0;
-    return (uint64_t)(v > 0 ? v : 16) << 20;
+    return (uint64_t)(v > 0 ? v : 0) << 20;
   }();
+  uint64_t total_ints = 0;
+  for (uint32_t i = 0; i < n_chunks; ++i) total_ints += h_chunks[i].n;
+  const uint64_t piece_ints =
+      forced_piece ? forced_piece
+                   : std::max<uint64_t>(16ull << 20, std::min<uint64_t>(64ull << 20, total_ints / 8));
   // (and at most 2^20 chunks, so batches of tiny chunks still pipeline)
   if (ordered) {
     uint64_t acc = 0;

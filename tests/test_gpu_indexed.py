@@ -247,3 +247,43 @@ def test_large_batch_shape():
     r = subprocess.run([sys.executable, "-c", _BIG.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("name", ["simdfastpfor-s4", "simdfastpfor", "simdbp128-s4"])
+def test_decode_phases_equal_one_call(cuda, name):
+    """izg_decode_ws_phase: the page index pass (phase 1) on a side stream,
+    then the decode (phase 2), gives izg_decode_ws's outputs, statuses and
+    words consumed — including under corruption; codecs without an index
+    pass do nothing in phase 1 and everything in phase 2."""
+    torch = cuda
+    codec = P.make_codec(name)
+    rng = np.random.default_rng(77)
+    for count in (40, 3000):  # split-decode and indexed-decode batch sizes
+        vals = [random_sorted(rng, 65536, int(rng.integers(1, 3000))) for _ in range(count)]
+        flat = np.concatenate(vals)
+        enc = H.encode_chunks(codec, flat, np.arange(count, dtype=np.uint64) * 65536,
+                              np.full(count, 65536, np.uint32))
+        w = enc.words.copy()
+        for _ in range(5):  # a few corrupted pages
+            t = enc.table[int(rng.integers(0, count))]
+            w[int(t["word_off"]) + int(rng.integers(0, int(t["n_words"])))] ^= np.uint32(1 << 7)
+        bad = P.Encoded(w, enc.table)
+        one = P.DeviceBatch(codec, bad)
+        two = P.DeviceBatch(codec, bad)
+        one.decode()
+        side = torch.cuda.Stream()
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        side.wait_event(ev)
+        two.decode_phase(1, side)
+        ev2 = torch.cuda.Event()
+        ev2.record(side)
+        torch.cuda.current_stream().wait_event(ev2)
+        two.decode_phase(2)
+        torch.cuda.synchronize()
+        assert np.array_equal(one.statuses(), two.statuses())
+        ok = one.statuses() == 0
+        assert ok.sum() >= count - 5
+        o1, o2 = one.output().reshape(count, 65536), two.output().reshape(count, 65536)
+        assert np.array_equal(o1[ok], o2[ok])
+        assert np.array_equal(one.consumed[:count].cpu().numpy(), two.consumed[:count].cpu().numpy())
