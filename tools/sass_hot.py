@@ -51,8 +51,12 @@ def main():
     ap.add_argument("--top", type=int, default=25)
     ap.add_argument("--dump")
     a = ap.parse_args()
+    seen = set()
     for name, rows in load(a.rep):
         tot = sum(n for _, _, n, _ in rows)
+        if (name, tot) in seen:  # ncu lists some kernels twice
+            continue
+        seen.add((name, tot))
         print(f"== {name[:150]}\n   instructions executed {tot:,} ({tot / a.units:.1f} per unit)")
         ops = collections.Counter()
         for _, src, n, _ in rows:
