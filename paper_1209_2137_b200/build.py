@@ -23,10 +23,10 @@ OBJDIR = os.path.join(LIBDIR, "obj")
 
 SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "decode_split.cu",
            "decode_group.cu", "decode_cta.cu", "intersect.cu", "host.cpp", "container.cpp"]
-# per-source extra flags: see the comment at the top of decode_scalar.cu
-SOURCE_FLAGS = {"decode_scalar.cu": ["-Xptxas", "-O1"]}
-if os.environ.get("IZG_SCALAR_O1", "1") == "0":  # sanitizer repro builds only
-    SOURCE_FLAGS = {}
+# per-source extra flags (none: decode_scalar.cu is built at -O3 again since
+# round 2, see the comment at its top); IZG_SCALAR_O1=1 restores the old
+# -Xptxas -O1 build of it for comparisons
+SOURCE_FLAGS = {"decode_scalar.cu": ["-Xptxas", "-O1"]} if os.environ.get("IZG_SCALAR_O1") == "1" else {}
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",

@@ -158,6 +158,11 @@ constexpr uint32_t kSplitMaxChunksBp = 384, kSplitMaxChunksFp = 1024;
 #define IZG_BIG_IDX_BATCH 24576
 #endif
 constexpr uint32_t kBigIdxBatch = IZG_BIG_IDX_BATCH;
+// SIMD-FastPFOR page index pass: one lane per page (1, default) or one warp
+// per page (0; round 1's kernel) — identical workspace contents.
+#ifndef IZG_INDEX_LANES
+#define IZG_INDEX_LANES 1
+#endif
 bool split_wanted(int codec, uint32_t n_chunks) {
   if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return false;
   static const int force = [] {
@@ -392,10 +397,17 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     }();
     (void)attr;
     ix = idx_view(d_ws, n_chunks);
-    const uint32_t g = (n_chunks + kIdxWarps - 1) / kIdxWarps;
-    auto* ifn = delta == IZG_DELTA_NONE ? fp_index_kernel<false, kVertical>
-                                        : fp_index_kernel<true, kVertical>;
-    ifn<<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks, n_chunks, ix);
+    if (IZG_INDEX_LANES) {  // one lane per page (index_fastpfor.cuh)
+      const uint32_t g = (n_chunks + 32 * kIdxLaneWarps - 1) / (32 * kIdxLaneWarps);
+      auto* lfn = delta == IZG_DELTA_NONE ? fp_index_lanes_kernel<false, kVertical>
+                                          : fp_index_lanes_kernel<true, kVertical>;
+      lfn<<<g, kIdxLaneWarps * 32, IdxLaneLayout::kSmem, s>>>(d_words, d_chunks, n_chunks, ix);
+    } else {
+      const uint32_t g = (n_chunks + kIdxWarps - 1) / kIdxWarps;
+      auto* ifn = delta == IZG_DELTA_NONE ? fp_index_kernel<false, kVertical>
+                                          : fp_index_kernel<true, kVertical>;
+      ifn<<<g, kIdxWarps * 32, IdxLayout::kSmem, s>>>(d_words, d_chunks, n_chunks, ix);
+    }
     if (phase == 1) return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
   } else if (idx) {
     ix = idx_view(d_ws, n_chunks);

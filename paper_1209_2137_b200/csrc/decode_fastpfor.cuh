@@ -346,8 +346,9 @@ static __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint
 #ifndef IZG_PATCH_SLOTS
 #define IZG_PATCH_SLOTS 2  // exceptions per lane per round (8 lanes per block)
 #endif
-// Vertical arrays (SIMD-FastPFOR): every address is formed from a valid
-// base, so no slot needs a select on its addresses — an idle slot (e >= c)
+// Lean patch (vertical arrays of SIMD-FastPFOR, scalar arrays of FastPFOR):
+// every address is formed from a valid base, so no slot needs a select on
+// its addresses — an idle slot (e >= c)
 // re-reads the block's exception 0, and a block without exceptions reads
 // width 0's base, which callers set to 0 (dir_base[0] = 0) — and the tile
 // address of position p in block q is built from per-lane constants (the
@@ -355,10 +356,11 @@ static __device__ int32_t fp_directory(FpScratch& sc, const uint32_t* page, uint
 #ifndef IZG_PATCH_LEAN
 #define IZG_PATCH_LEAN 1
 #endif
-__device__ __forceinline__ bool fp_patch_vertical(uint32_t t, const uint32_t* page,
-                                                  const uint8_t* ba, uint32_t myb, uint32_t myw,
-                                                  uint32_t myc, uint32_t mybp, uint32_t mycur,
-                                                  uint32_t mybase, int lane) {
+template <int ST>
+__device__ __forceinline__ bool fp_patch_lean(uint32_t t, const uint32_t* page,
+                                              const uint8_t* ba, uint32_t myb, uint32_t myw,
+                                              uint32_t myc, uint32_t mybp, uint32_t mycur,
+                                              uint32_t mybase, int lane) {
   const uint32_t q = (lane >> 3) & 3u, s8 = lane & 7;
   uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));
   mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));
@@ -375,12 +377,21 @@ __device__ __forceinline__ bool fp_patch_vertical(uint32_t t, const uint32_t* pa
       const uint32_t e = e0 + 8u * j;
       ok[j] = e < myc;
       const uint32_t rr = mycur + (ok[j] ? e : 0u);
-      const uint32_t tt = rr & 127u, bit = (tt >> 2) * myw;
-      const uint32_t word = (rr >> 7) * w4 + 4u * (bit >> 5) + (tt & 3u);
-      sh[j] = bit & 31u;
+      uint32_t word, step;
+      if (ST == kVertical) {  // group r/128, lane r%4, slot (r%128)/4
+        const uint32_t tt = rr & 127u, bit = (tt >> 2) * myw;
+        word = (rr >> 7) * w4 + 4u * (bit >> 5) + (tt & 3u);
+        sh[j] = bit & 31u;
+        step = 4u;
+      } else {  // group r/32, bits [(r%32)*w, +w) of its w-word stream
+        const uint32_t bit = (rr & 31u) * myw;
+        word = (rr >> 5) * myw + (bit >> 5);
+        sh[j] = bit & 31u;
+        step = 1u;
+      }
       pp[j] = ok[j] ? ld_u8(pb + e) : 0u;
       lo[j] = ld_u32(arr + word);
-      hi[j] = ld_u32(arr + word + (sh[j] + myw > 32 ? 4u : 0u));
+      hi[j] = ld_u32(arr + word + (sh[j] + myw > 32 ? step : 0u));
     }
 #pragma unroll
     for (int j = 0; j < IZG_PATCH_SLOTS; ++j) {
@@ -405,8 +416,7 @@ __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const
                                          uint32_t myb, uint32_t myw, uint32_t myc, uint32_t mybp,
                                          uint32_t mycur, uint32_t mybase, int lane) {
 #if IZG_PATCH_LEAN
-  if constexpr (ST == kVertical)
-    return fp_patch_vertical(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
+  return fp_patch_lean<ST>(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
 #endif
   const uint32_t q = (lane >> 3) & 3u, s8 = lane & 7;
   uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));

@@ -1,18 +1,18 @@
 // decode_scalar.cu — the scalar-array FastPFOR decode kernels
 // (codec_patched.cpp:292-417, PatchStorage::scalar_arrays), in their own
-// translation unit so build.py can compile them with ptxas -O1.
+// translation unit.
 //
-// Why: built at ptxas -O2/-O3 (this library's default), these kernels faulted
-// with "misaligned address" / "illegal memory access" on pages with
+// History: in round 1 these kernels, built at ptxas -O2/-O3,
+// faulted ("misaligned address" / "illegal memory access") on pages with
 // exceptions — deterministically, e.g. any single 128-integer page with one
-// exception at b = 3 (tests/test_collisions.py reproduces it) — while the same
-// source at -O0/-O1, or with any change to the exception loop (a printf, no
-// inlining, dropping either its loads or its shared-memory ORs), decoded
-// exactly.  Every address the loop forms was checked in range and aligned in
-// an instrumented build, and the vertical-array instantiation of the same
-// code (SIMD-FastPFOR) is unaffected.  Without a faulting PC in this sandbox
-// (no compute-sanitizer, no core dumps) the cause is not pinned down;
-// DESIGN.md §9 records it.
+// exception at b = 3 (tools/repro_scalar_fault.py) — while -O0/-O1 or any
+// change to the exception loop decoded exactly; this file was built at
+// -Xptxas -O1.  Round 2 replaced the patch loop by the lean one
+// (decode_fastpfor.cuh: fp_patch_lean — every address from a valid base,
+// no address selects), and at -O3 the repro, tests/test_collisions.py and
+// tests/test_gpu_f3.py pass; the special build flag is gone.  The fault's
+// root cause was never pinned down (the pool refuses compute-sanitizer and
+// GPU core dumps).
 #include "decode_kernel.cuh"
 
 namespace izg {

@@ -179,6 +179,158 @@ __global__ void __launch_bounds__(kIdxWarps * 32)
   if (lane == 0) ix.hdr[c] = make_uint4((uint32_t)st | parsed << 8, A + 1 + (uint32_t)ba_words, end, A);
 }
 
+// ---- lane-per-page index pass (round 2) -------------------------------------
+//
+// The warp-per-page pass above spends ~132 warp-instructions per 512
+// integers, mostly on the windowed walk: per 128-byte window every lane
+// decodes speculative entry lengths at four byte offsets, and the chain of
+// entry starts is serial anyway.  Here each LANE indexes its own page: the
+// byte-array walk is a serial loop of a handful of instructions per entry
+// (codec_patched.cpp:309-336, every check in the reference's order), so a
+// warp walks 32 pages at once and the pass costs a few instructions per 512
+// integers; its time is the memory latency of the 32 walks, hidden by the
+// warps resident on the SM.  The exception directory (:338-379) is read
+// first (its errors still rank after the walk's, as in the reference); each
+// block's cursor in its width array is a running count per width, kept per
+// lane in shared memory ([width][lane]: conflict-free); the block loop's
+// overrun / exhaustion checks (:387-388, 406-407) and the packed-size check
+// are made during the walk.  Output: the same header, directory and block
+// records as fp_index_kernel, so the decode kernel is unchanged.
+constexpr int kIdxLaneWarps = 4;
+struct IdxLaneLayout {
+  // per warp: running counts cnt[33][32], array sizes nn[33][32] (u32)
+  static constexpr uint32_t kWarpBytes = 2 * 33 * 32 * 4;
+  static constexpr size_t kSmem = kIdxLaneWarps * kWarpBytes;
+};
+
+template <bool ARRAY, int ST>
+__global__ void __launch_bounds__(kIdxLaneWarps * 32)
+    fp_index_lanes_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
+                          uint32_t n_chunks, IdxView ix) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(smem + warp * IdxLaneLayout::kWarpBytes);
+  uint32_t* nn = cnt + 33 * 32;
+  const uint32_t c = (blockIdx.x * kIdxLaneWarps + warp) * 32u + lane;
+  if (c >= n_chunks) return;  // the lanes work independently from here on
+  const izg_chunk ch = chunks[c];
+  // decode_array's length check or decode_deltas' count checks: the decode
+  // kernel repeats them and never reads this page's record when they fail
+  if (ARRAY ? (ch.n == 0 || ch.n > IZG_CHUNK_SIZE) : (ch.n % 128 || ch.n > IZG_CHUNK_SIZE)) {
+    ix.hdr[c] = make_uint4(IZG_OK, 0, 0, 0);
+    return;
+  }
+  const uint32_t nblocks = (ARRAY ? ch.n / 128 * 128 : ch.n) / 128;
+  const uint32_t* page = words + ch.word_off;
+  const uint32_t nw = ch.n_words;
+  if (nblocks == 0) {  // decode_deltas(count == 0) reads nothing (codec_patched.cpp:295)
+    ix.hdr[c] = make_uint4(IZG_OK, 0, 0, 0);
+    return;
+  }
+  const uint32_t A = nw ? __ldg(page) : 0u;
+  const uint32_t L = (nw && A >= 1 && A < nw) ? __ldg(page + A) : 0u;
+  const uint64_t ba_words = ((uint64_t)L + 3) / 4;
+  int32_t hst = IZG_OK;
+  if (nw == 0) hst = IZG_E_FP_TRUNC_PAGE;
+  else if (A < 1 || A >= nw) hst = IZG_E_FP_BA_OFFSET;
+  else if (A + 1 + ba_words > nw) hst = IZG_E_FP_TRUNC_BA;
+  if (hst) {
+    ix.hdr[c] = make_uint4((uint32_t)hst, 0, 0, 0);
+    return;
+  }
+  // exception directory (codec_patched.cpp:339-379); its error, if any, is
+  // reported only after the byte-array walk has passed
+  int32_t dst = IZG_OK;
+  uint64_t pos = A + 1 + ba_words;
+  uint32_t* dir = ix.dir + (size_t)c * 32;
+  for (uint32_t w = 0; w <= 32; ++w) nn[w * 32 + lane] = 0;
+  uint32_t bits = 0;
+  if (pos >= nw) {
+    dst = IZG_E_FP_NO_BITSET;
+  } else {
+    bits = __ldg(page + pos);
+    ++pos;
+  }
+  for (uint32_t w = 1; w <= 32; ++w) {
+    uint32_t base = 0;
+    if (dst == IZG_OK && ((bits >> (w - 1)) & 1u)) {
+      if (pos >= nw) {
+        dst = IZG_E_FP_TRUNC_EXC;
+      } else {
+        const uint32_t n = __ldg(page + pos);
+        uint64_t nwords;
+        if (ST == kVertical) {
+          pos = (pos + 1 + 3) & ~uint64_t{3};  // 16-byte alignment in the page
+          nwords = ((uint64_t)n + 127) / 128 * 4 * w;
+        } else {
+          pos = pos + 1;
+          nwords = ((uint64_t)n + 31) / 32 * w;
+        }
+        if (pos + nwords > nw) {
+          dst = IZG_E_FP_TRUNC_EXC;
+        } else {
+          base = (uint32_t)pos;
+          nn[w * 32 + lane] = n;
+          pos += nwords;
+        }
+      }
+    }
+    dir[w - 1] = dst == IZG_OK ? base : 0u;
+  }
+  const uint32_t end = (uint32_t)pos;
+  // the byte-array walk (codec_patched.cpp:309-336) with every block's record
+  for (uint32_t w = 0; w <= 32; ++w) cnt[w * 32 + lane] = 0;
+  const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
+  const uint32_t Lc = L > 0x7FFFFFF0u ? 0x7FFFFFF0u : L;
+  uint4* rec = ix.page_rec(c);
+  int32_t wst = IZG_OK, lst = IZG_OK;  // walk error; first block-loop error
+  uint32_t s = 0, packed = 1, k = 0;
+  for (; k < nblocks; ++k) {
+    if (s + 2 > Lc) {
+      wst = IZG_E_FP_TRUNC_META;
+      break;
+    }
+    const uint32_t b = __ldg(ba + s), mb = __ldg(ba + s + 1);
+    if (b > 32 || mb > 32 || b > mb) {
+      wst = IZG_E_FP_WIDTHS;
+      break;
+    }
+    uint32_t e = b, cc = 0, cur = 0;
+    if (mb > b) {
+      if (s + 2 >= Lc) {
+        wst = IZG_E_FP_TRUNC_META;
+        break;
+      }
+      cc = __ldg(ba + s + 2);
+      if (cc == 0) {
+        wst = IZG_E_FP_EMPTY_EXC;
+        break;
+      }
+      if (s + 3 + cc > Lc) {
+        wst = IZG_E_FP_TRUNC_POS;
+        break;
+      }
+      const uint32_t w = mb - b;
+      cur = cnt[w * 32 + lane];
+      cnt[w * 32 + lane] = cur + cc;
+      e = b | w << 6 | cc << 12;
+      if (lst == IZG_OK && (uint64_t)cur + cc > nn[w * 32 + lane] && packed + 4 * b <= A)
+        lst = IZG_E_FP_EXHAUSTED;
+    }
+    if (lst == IZG_OK && packed + 4 * b > A) lst = IZG_E_FP_OVERRUN;
+    stg128_cg(rec + k, make_uint4(e, packed, s + 3, cur));
+    packed += 4 * b;
+    s += cc ? 3 + cc : 2;
+  }
+  int32_t st = wst;
+  if (st == IZG_OK && s != L) st = IZG_E_FP_BA_LEN;
+  const bool dir_ok = st == IZG_OK && dst == IZG_OK;  // fp_index_kernel reports `end` only then
+  if (st == IZG_OK) st = dst;
+  if (st == IZG_OK) st = lst;
+  if (st == IZG_OK && packed != A) st = IZG_E_FP_PACKED_SIZE;
+  ix.hdr[c] = make_uint4((uint32_t)st | k << 8, A + 1 + (uint32_t)ba_words, dir_ok ? end : 0u, A);
+}
+
 // ---- decode side -----------------------------------------------------------
 
 // Error paths: does any exception position of records [0, nb) reach 128
