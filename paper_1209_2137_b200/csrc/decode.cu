@@ -158,10 +158,14 @@ constexpr uint32_t kSplitMaxChunksBp = 384, kSplitMaxChunksFp = 1024;
 #define IZG_BIG_IDX_BATCH 24576
 #endif
 constexpr uint32_t kBigIdxBatch = IZG_BIG_IDX_BATCH;
-// SIMD-FastPFOR page index pass: one lane per page (1, default) or one warp
-// per page (0; round 1's kernel) — identical workspace contents.
-#ifndef IZG_INDEX_LANES
-#define IZG_INDEX_LANES 1
+// SIMD-FastPFOR page index pass: one lane per page from IZG_INDEX_LANES_MIN
+// pages on, one warp per page below (identical workspace contents).  The
+// lane walk is latency-bound (~0.35 ms whatever the batch up to ~8,192
+// pages), the warp walk issue-bound: measured (tools/index_probe.py, C5
+// pages, ms, lane / warp): 2,048: 0.35 / 0.08; 8,192: 0.36 / 0.19; 32,768:
+// 0.44 / 0.62; 65,536: 0.90 / 1.19.  IZG_INDEX_LANES_MIN=0 / huge forces it.
+#ifndef IZG_INDEX_LANES_MIN
+#define IZG_INDEX_LANES_MIN 16384
 #endif
 bool split_wanted(int codec, uint32_t n_chunks) {
   if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return false;
@@ -397,7 +401,11 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     }();
     (void)attr;
     ix = idx_view(d_ws, n_chunks);
-    if (IZG_INDEX_LANES) {  // one lane per page (index_fastpfor.cuh)
+    static const uint32_t lanes_min = [] {  // IZG_INDEX_LANES_MIN: tests / tuning
+      const char* e = std::getenv("IZG_INDEX_LANES_MIN");
+      return e ? (uint32_t)std::strtoul(e, nullptr, 10) : (uint32_t)IZG_INDEX_LANES_MIN;
+    }();
+    if (n_chunks >= lanes_min) {  // one lane per page (index_fastpfor.cuh)
       const uint32_t g = (n_chunks + 32 * kIdxLaneWarps - 1) / (32 * kIdxLaneWarps);
       auto* lfn = delta == IZG_DELTA_NONE ? fp_index_lanes_kernel<false, kVertical>
                                           : fp_index_lanes_kernel<true, kVertical>;

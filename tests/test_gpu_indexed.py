@@ -249,6 +249,25 @@ def test_large_batch_shape():
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
+@pytest.mark.parametrize("env", [{"IZG_INDEX_LANES_MIN": "0", "IZG_SPLIT": "0"},
+                                 {"IZG_INDEX_LANES_MIN": "0", "IZG_SPLIT": "1"}],
+                         ids=["indexed", "split"])
+def test_lane_index_pass(env):
+    """The lane-per-page index pass (fp_index_lanes_kernel, taken from
+    IZG_INDEX_LANES_MIN pages on) forced onto the small batches of this file
+    — every structural mutation, random fuzz and raw case — in front of the
+    indexed decode and of the split decode: statuses and outputs against the
+    oracle and the fused path, as with the warp-per-page pass."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _BIG.format(root=root)],
+                       env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
 @pytest.mark.parametrize("name", ["simdfastpfor-s4", "simdfastpfor", "simdbp128-s4"])
 def test_decode_phases_equal_one_call(cuda, name):
     """izg_decode_ws_phase: the page index pass (phase 1) on a side stream,
