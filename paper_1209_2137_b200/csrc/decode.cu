@@ -97,6 +97,26 @@ GroupFn pick_group(int kw, int delta);
 GroupFn pick_cta(int delta);
 size_t cta_smem_bytes();
 int cta_threads();
+// Team SIMD-FastPFOR decode (one CTA per page, indexed path): decode_team.cu.
+using TeamFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
+                        uint32_t*, uint32_t*, const CUtensorMap, int, IdxView);
+TeamFn pick_team(int delta);
+size_t team_smem_bytes();
+int team_threads();
+
+// Indexed SIMD-FastPFOR batches of at least IZG_TEAM_MIN pages decode with
+// the team kernel (team.cuh).  IZG_TEAM=0 / 1 forces it off / on.
+#ifndef IZG_TEAM_MIN
+#define IZG_TEAM_MIN 0xFFFFFFFFu
+#endif
+bool team_wanted(uint32_t n_chunks) {
+  static const int force = [] {
+    const char* e = std::getenv("IZG_TEAM");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (force >= 0) return force != 0;
+  return n_chunks >= IZG_TEAM_MIN;
+}
 
 // SIMD-BP128 array-mode batches of up to IZG_CTA_MAX chunks take the
 // CTA-cooperative kernel (cta.cuh): with fewer chunks than ~2 per resident
@@ -197,7 +217,7 @@ struct DeviceInfo {
   int sms = 0;
   // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink,
   //  + 3 kCodecs: split kernels, 4 kCodecs + 0..2: group kernels KW = 2, 4, 8)][delta]
-  int occ[4 * kCodecs + 5][5] = {};  // + 4 kCodecs + 3: big indexed, + 4: CTA kernel
+  int occ[4 * kCodecs + 6][5] = {};  // + 4 kCodecs + 3: big indexed, + 4: CTA kernel, + 5: team
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -421,6 +441,23 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     ix = idx_view(d_ws, n_chunks);
   }
   if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
+  if (idx && !split && team_wanted(n_chunks)) {
+    TeamFn tfn = pick_team(delta);
+    int tper_sm = 0, tsms = 0;
+    uint32_t* tcounter = nullptr;
+    rc = prepare(dev, 4 * kCodecs + 5, delta, reinterpret_cast<const void*>(tfn), team_threads(),
+                 team_smem_bytes(), &tper_sm, &tsms, &tcounter);
+    if (rc != IZG_SUCCESS) return rc;
+    if (cudaMemsetAsync(tcounter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
+    const uint32_t grid = (uint32_t)std::min<uint64_t>(n_chunks, (uint64_t)tper_sm * tsms);
+    CUtensorMap omap;
+    std::memset(&omap, 0, sizeof(omap));
+    const int tma_out = IZG_TMA_STORE && make_out_map(&omap, d_out) ? 1 : 0;
+    tfn<<<grid, team_threads(), team_smem_bytes(), s>>>(d_words, d_chunks, n_chunks, d_out,
+                                                        d_status, d_consumed, tcounter, omap,
+                                                        tma_out, ix);
+    return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+  }
   if (split) {
     SplitArgs sa;
     sa.seg = reinterpret_cast<SegState*>(static_cast<uint8_t*>(d_ws) +

@@ -1,0 +1,25 @@
+// decode_team.cu — instantiations of the team SIMD-FastPFOR decode of
+// team.cuh (one CTA of 8 warps per page, shared TMA staging, windowed bulk
+// unpack of the exception arrays, two-level prefix sum).
+#include "team.cuh"
+
+namespace izg {
+
+using TeamFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
+                        uint32_t*, uint32_t*, const CUtensorMap, int, IdxView);
+
+TeamFn pick_team(int delta) {
+  switch (delta) {
+    case IZG_DELTA_NONE: return fp_team_kernel<IZG_DELTA_NONE>;
+    case IZG_DELTA_D1: return fp_team_kernel<IZG_DELTA_D1>;
+    case IZG_DELTA_D4: return fp_team_kernel<IZG_DELTA_D4>;
+    case IZG_DELTA_D2: return fp_team_kernel<IZG_DELTA_D2>;
+    case IZG_DELTA_DM: return fp_team_kernel<IZG_DELTA_DM>;
+  }
+  return nullptr;
+}
+
+size_t team_smem_bytes() { return TeamLayout::kSmem; }
+int team_threads() { return kTeamWarps * 32; }
+
+}  // namespace izg

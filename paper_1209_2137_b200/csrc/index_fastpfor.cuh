@@ -24,6 +24,10 @@
 //   dir[n][32]    uint32 base word of exception array w (index w-1)
 //   rec[n][512]   uint4 per block {b | w<<6 | c<<12, packed word, first
 //                 position byte (byte-array offset), cursor in array w}
+//   snap[n][16][32] uint16 cursor of every width (index w-1) after each 32
+//                 blocks (row j: after block 32 (j + 1), or the page's last),
+//                 for the team decode's exception windows (team.cuh); bit 31
+//                 of hdr.x is set when a cursor passed 65,535 (rows invalid)
 #pragma once
 #include "decode_fastpfor.cuh"
 #include "izg_common.cuh"
@@ -36,13 +40,14 @@ struct IdxView {
   uint4* hdr;
   uint32_t* dir;
   uint4* rec;
+  uint16_t* snap;
   __device__ __forceinline__ uint4* page_rec(uint32_t c) const {
     return rec + (size_t)c * kMaxBlocks;
   }
 };
 
 __host__ __device__ inline uint64_t idx_workspace_bytes(uint32_t n_chunks) {
-  return (uint64_t)n_chunks * (16u + 32u * 4u + kMaxBlocks * 16u);
+  return (uint64_t)n_chunks * (16u + 32u * 4u + kMaxBlocks * 16u + 16u * 32u * 2u);
 }
 
 __host__ __device__ inline IdxView idx_view(void* ws, uint32_t n_chunks) {
@@ -51,6 +56,7 @@ __host__ __device__ inline IdxView idx_view(void* ws, uint32_t n_chunks) {
   v.hdr = reinterpret_cast<uint4*>(p);
   v.dir = reinterpret_cast<uint32_t*>(p + (size_t)n_chunks * 16u);
   v.rec = reinterpret_cast<uint4*>(p + (size_t)n_chunks * (16u + 128u));
+  v.snap = reinterpret_cast<uint16_t*>(p + (size_t)n_chunks * (16u + 128u + kMaxBlocks * 16u));
   return v;
 }
 
@@ -60,12 +66,14 @@ __host__ __device__ inline IdxView idx_view(void* ws, uint32_t n_chunks) {
 // plus the warp's running per-width count `cnt`), and — when `checks` — the
 // block loop's overrun / exhaustion checks in block order
 // (codec_patched.cpp:387-388, 406-407).  Records go out coalesced.
-static __device__ int32_t fp_meta(const FpScratch& sc, uint32_t* cnt, uint4* rec, uint32_t nb,
-                           uint32_t A, bool checks, int lane, uint32_t* packed_end) {
+static __device__ int32_t fp_meta(const FpScratch& sc, uint32_t* cnt, uint4* rec, uint16_t* snap,
+                           uint32_t nb, uint32_t A, bool checks, int lane, uint32_t* packed_end,
+                           bool* cursor_ovf) {
   cnt[lane + 1] = 0;
   __syncwarp();
   uint32_t packed = 1, bpos = 0;
   int32_t err = IZG_OK;
+  bool ovf = false;
 #pragma unroll 1
   for (uint32_t j0 = 0; j0 < nb; j0 += 32) {
     const uint32_t k = j0 + lane;
@@ -85,6 +93,11 @@ static __device__ int32_t fp_meta(const FpScratch& sc, uint32_t* cnt, uint4* rec
     __syncwarp();
     if (c && lane == 31 - __clz(grp)) cnt[w] = cur + c;  // last block of its width
     __syncwarp();
+    {  // every width's cursor after this step (team.cuh's exception windows)
+      const uint32_t cv = cnt[lane + 1];
+      ovf |= cv > 65535u;
+      snap[(j0 >> 5) * 32 + lane] = (uint16_t)min(cv, 65535u);
+    }
     if (checks && err == IZG_OK) {
       const bool ov = live && packed + inc.x > A;
       const bool ex = c && (uint64_t)cur + c > sc.dir_n[w];
@@ -99,6 +112,7 @@ static __device__ int32_t fp_meta(const FpScratch& sc, uint32_t* cnt, uint4* rec
     bpos += __shfl_sync(0xFFFFFFFFu, inc.y, 31);
   }
   *packed_end = packed;
+  *cursor_ovf = __any_sync(0xFFFFFFFFu, ovf);
   return err;
 }
 
@@ -174,9 +188,13 @@ __global__ void __launch_bounds__(kIdxWarps * 32)
     if (st == IZG_OK) ix.dir[(size_t)c * 32 + lane] = sc.dir_base[lane + 1];
   }
   uint32_t packed = 0;
-  const int32_t bst = fp_meta(sc, cnt, ix.page_rec(c), parsed, A, st == IZG_OK, lane, &packed);
+  bool ovf = false;
+  const int32_t bst = fp_meta(sc, cnt, ix.page_rec(c), ix.snap + (size_t)c * 512, parsed, A,
+                              st == IZG_OK, lane, &packed, &ovf);
   if (st == IZG_OK) st = bst ? bst : (packed != A ? IZG_E_FP_PACKED_SIZE : IZG_OK);
-  if (lane == 0) ix.hdr[c] = make_uint4((uint32_t)st | parsed << 8, A + 1 + (uint32_t)ba_words, end, A);
+  if (lane == 0)
+    ix.hdr[c] = make_uint4((uint32_t)st | parsed << 8 | (ovf ? 0x80000000u : 0u),
+                           A + 1 + (uint32_t)ba_words, end, A);
 }
 
 // ---- lane-per-page index pass (round 2) -------------------------------------
@@ -299,6 +317,8 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
   uint4* rec = ix.page_rec(c);
   int32_t wst = IZG_OK, lst = IZG_OK;  // walk error; first block-loop error
   uint32_t s = 0, packed = 1, k = 0;
+  bool ovf = false;  // a cursor passed 65,535 (snapshot rows are 16-bit)
+  uint4* snap = reinterpret_cast<uint4*>(ix.snap + (size_t)c * 512);
 #pragma unroll
   for (uint32_t a = 0; a < kIdxLaneAhead; a += 128)
     if (a < Lc) asm volatile("prefetch.global.L1 [%0];" ::"l"(ba + a));
@@ -344,6 +364,7 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
       const uint32_t w = mb - b;
       cur = cnt[w * 32 + lane];
       cnt[w * 32 + lane] = cur + cc;
+      ovf |= cur + cc > 65535u;
       e = b | w << 6 | cc << 12;
       if (lst == IZG_OK && (uint64_t)cur + cc > nn[w * 32 + lane] && packed + 4 * b <= A)
         lst = IZG_E_FP_EXHAUSTED;
@@ -352,6 +373,18 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
     stg128_cg(rec + k, make_uint4(e, packed, s + 3, cur));
     packed += 4 * b;
     s += cc ? 3 + cc : 2;
+    if ((k & 31u) == 31u || k + 1 == nblocks) {  // cursors after 32 (k / 32 + 1) blocks
+#pragma unroll
+      for (uint32_t w4 = 0; w4 < 4; ++w4) {
+        uint32_t x[4];
+#pragma unroll
+        for (uint32_t j = 0; j < 4; ++j) {
+          const uint32_t w = 8 * w4 + 2 * j + 1;  // widths w, w + 1 -> one word
+          x[j] = min(cnt[w * 32 + lane], 65535u) | min(cnt[(w + 1) * 32 + lane], 65535u) << 16;
+        }
+        stg128_cg(snap + (k >> 5) * 4 + w4, make_uint4(x[0], x[1], x[2], x[3]));
+      }
+    }
   }
   int32_t st = wst;
   if (st == IZG_OK && s != L) st = IZG_E_FP_BA_LEN;
@@ -359,7 +392,8 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
   if (st == IZG_OK) st = dst;
   if (st == IZG_OK) st = lst;
   if (st == IZG_OK && packed != A) st = IZG_E_FP_PACKED_SIZE;
-  ix.hdr[c] = make_uint4((uint32_t)st | k << 8, A + 1 + (uint32_t)ba_words, dir_ok ? end : 0u, A);
+  ix.hdr[c] = make_uint4((uint32_t)st | k << 8 | (ovf ? 0x80000000u : 0u),
+                         A + 1 + (uint32_t)ba_words, dir_ok ? end : 0u, A);
 }
 
 // ---- decode side -----------------------------------------------------------
@@ -467,8 +501,8 @@ __device__ int32_t fastpfor_core_idx(WarpRing& r, OS& os, uint32_t* dir_base,
   if (st) {
     if (st == IZG_E_FP_TRUNC_PAGE || st == IZG_E_FP_BA_OFFSET || st == IZG_E_FP_TRUNC_BA)
       return st;
-    return fp_positions_bad_idx(rec, reinterpret_cast<const uint8_t*>(page + h.w + 1), h.x >> 8,
-                                lane)
+    return fp_positions_bad_idx(rec, reinterpret_cast<const uint8_t*>(page + h.w + 1),
+                                (h.x >> 8) & 0xFFFFu, lane)
                ? IZG_E_FP_POS_RANGE
                : st;
   }

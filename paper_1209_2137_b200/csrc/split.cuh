@@ -382,7 +382,7 @@ __global__ void __launch_bounds__((Layout<CODEC, CODEC == IZG_SIMDFASTPFOR>::kWa
           int32_t e = hs;
           if (hs != IZG_E_FP_TRUNC_PAGE && hs != IZG_E_FP_BA_OFFSET && hs != IZG_E_FP_TRUNC_BA &&
               fp_positions_bad_idx(ix.page_rec(c), reinterpret_cast<const uint8_t*>(p + hdr.w + 1),
-                                   hdr.x >> 8, lane))
+                                   (hdr.x >> 8) & 0xFFFFu, lane))
             e = IZG_E_FP_POS_RANGE;
           if (lane == 0) {
             status[c] = e;

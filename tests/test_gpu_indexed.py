@@ -214,8 +214,8 @@ def test_workspace_too_small_falls_back_to_fused(cuda):
     # small ones add the split kernel's look-back state (test_gpu_split.py)
     n = 1 << 14
     assert N.lib().izg_decode_workspace_size(0, n) == 0
-    assert N.lib().izg_decode_workspace_size(1, n) == n * (16 + 128 + 512 * 16)
-    assert N.lib().izg_decode_workspace_size(1, 100) > 100 * (16 + 128 + 512 * 16)
+    assert N.lib().izg_decode_workspace_size(1, n) == n * (16 + 128 + 512 * 16 + 1024)
+    assert N.lib().izg_decode_workspace_size(1, 100) > 100 * (16 + 128 + 512 * 16 + 1024)
 
 
 _BIG = r'''
