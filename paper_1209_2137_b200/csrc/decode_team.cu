@@ -20,6 +20,18 @@ TeamFn pick_team(int delta) {
 }
 
 size_t team_smem_bytes() { return TeamLayout::kSmem; }
-int team_threads() { return kTeamWarps * 32; }
+int team_threads() { return kTeamThreads; }
 
 }  // namespace izg
+
+#ifdef IZG_TEAM_PROF
+extern "C" int izg_debug_team_prof(void* host, int reset) {
+  if (cudaMemcpyFromSymbol(host, izg::g_team_prof, sizeof(izg::g_team_prof)) != cudaSuccess) return -1;
+  if (reset) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, izg::g_team_prof) != cudaSuccess) return -1;
+    cudaMemset(p, 0, sizeof(izg::g_team_prof));
+  }
+  return 0;
+}
+#endif

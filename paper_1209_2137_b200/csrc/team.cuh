@@ -54,10 +54,27 @@ constexpr uint32_t kTeamPs = 5 * 1024;        // position bytes staging
 constexpr uint32_t kTeamXb = IZG_TEAM_XB;     // unpacked exception highs of a window
 constexpr uint32_t kTeamXGroups = kTeamXb / 512;
 #ifndef IZG_TEAM_UNPACK
-#define IZG_TEAM_UNPACK team_unpack_rows  // or team_unpack_window
+#define IZG_TEAM_UNPACK team_unpack_window  // or team_unpack_rows (more row loads, fewer moves)
+#endif
+#ifndef IZG_TEAM_AHEAD
+#define IZG_TEAM_AHEAD 2  // warp 0 stages more once fewer than this many lie ahead
 #endif
 #ifndef IZG_TEAM_MINCTAS
 #define IZG_TEAM_MINCTAS 3  // CTAs per SM the register allocation allows for
+#endif
+constexpr int kTeamThreads = (kTeamWarps + 1) * 32;  // 8 decoding warps + the staging warp
+#define IZG_TEAM_LB_THREADS ((kTeamWarps + 1) * 32)
+
+#ifdef IZG_TEAM_PROF  // developer build: where a page's time goes (cycles, summed over pages)
+// [0] pages, [1] claim -> setup barrier, [2] setup barrier -> first staging landed (warp 0),
+// [3] window set-ups (warp 0, incl. barriers), [4] iterations (warp 0), [5] loop end -> page end
+// [6] warp 0: waits on `full`, [7] warp 0: waits on the carry mailbox
+__device__ unsigned long long g_team_prof[8];
+#define TEAM_PROF_T(x) const long long x = clock64()
+#define TEAM_PROF_ADD(i, v) atomicAdd(&g_team_prof[i], (unsigned long long)(v))
+#else
+#define TEAM_PROF_T(x)
+#define TEAM_PROF_ADD(i, v)
 #endif
 
 struct TeamLayout {
@@ -69,11 +86,13 @@ struct TeamLayout {
   static constexpr uint32_t kSnap = kXb + kTeamXb;       // u16 [16][32]
   static constexpr uint32_t kXrel = kSnap + 1024;        // i32 [36]
   static constexpr uint32_t kDirb = kXrel + 36 * 4;      // u32 [36]
-  static constexpr uint32_t kTot = kDirb + 36 * 4;       // uint4 [2][warps]
-  static constexpr uint32_t kInfo = kTot + 2 * kTeamWarps * 16;  // uint2 [slots] {pkrel, psrel}
+  static constexpr uint32_t kTot = kDirb + 36 * 4;       // uint4 [warps + 1]: carry mailboxes, final carry
+  static constexpr uint32_t kInfo = kTot + (kTeamWarps + 1) * 16;  // uint2 [slots] {pkrel, psrel}
   static constexpr uint32_t kAlloc = kInfo + kTeamSlots * 8;     // uint2 [slots] {pk off, ps off}
-  static constexpr uint32_t kBar = kAlloc + kTeamSlots * 8;      // u64 [slots]
-  static constexpr uint32_t kPage = kBar + kTeamSlots * 8;       // u32 page, u32 bad flag
+  static constexpr uint32_t kBar = kAlloc + kTeamSlots * 8;      // u64 [slots]: staging landed
+  static constexpr uint32_t kEmpty = kBar + kTeamSlots * 8;      // u64 [slots]: staging read by all warps
+  static constexpr uint32_t kMbx = kEmpty + kTeamSlots * 8;      // u64 [warps]: mailbox posted
+  static constexpr uint32_t kPage = kMbx + kTeamWarps * 8;       // u32 page, u32 bad flag
   static constexpr size_t kSmem = kPage + 16;
 };
 static_assert(TeamLayout::kXrel % 16 == 0 && TeamLayout::kTot % 16 == 0, "team layout");
@@ -326,9 +345,25 @@ __device__ __forceinline__ void team_scan_apply(uint32_t (&v)[4][4], const uint4
 // Producer state of a page (warp 0; lane 0 issues the copies).
 struct TeamProducer {
   uint32_t issued;            // super-iterations of this page staged so far
+  uint32_t done;              // super-iterations every warp has finished reading
   uint32_t pk_head, ps_head;  // allocation heads of the two staging buffers
   uint64_t policy;
 };
+
+__device__ __forceinline__ bool mbar_test_s(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive_s(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 
 // Place `len` bytes in a staging buffer of `size` whose unconsumed data
 // spans [tail, head) in allocation order (tail == 0xFFFFFFFF: nothing in
@@ -343,75 +378,94 @@ __device__ __forceinline__ uint32_t team_place(uint32_t head, uint32_t tail, uin
   return head + len <= tail ? head : 0xFFFFFFFFu;
 }
 
-// Stage super-iterations while they fit: up to kTeamSlots beyond the `done`
-// consumed ones.  All lanes of warp 0 call (the bounds live in lanes 0..16);
-// lane 0 allocates and issues.  Per super-iteration j: the packed words
+// Stage super-iterations until number `need` is staged, and beyond it while
+// they fit, up to kTeamSlots past the `done` consumed ones.  All lanes of
+// warp 0 call (the bounds live in lanes 0..16); lane 0 allocates and issues.
+// A super-iteration counts as consumed once every warp has arrived on its
+// slot's `empty` barrier.  Per super-iteration j: the packed words
 // [P_j, P_j+1), its block records, and the byte-array bytes [S_j, S_j+1)
 // (skipped when they exceed the buffer: that super-iteration patches from
 // global memory), each as the 16-byte-aligned span covering it, all
-// completing on the slot's mbarrier.  info[slot] = {shared address of page
-// word 0, shared address of byte-array byte 0 (0: not staged)}.
+// completing on the slot's `full` barrier.  info[slot] = {shared address of
+// page word 0, shared address of byte-array byte 0 (0: not staged)}.
 __device__ __forceinline__ void team_produce(TeamProducer& pr, uint32_t sb, uint32_t git0,
-                                             uint32_t done, uint32_t K, uint32_t nb, uint32_t bP,
+                                             uint32_t need, uint32_t K, uint32_t nb, uint32_t bP,
                                              uint32_t bS, const uint32_t* page, const uint8_t* ba,
                                              const uint4* rec, int lane) {
   using LY = TeamLayout;
-  while (pr.issued < K && pr.issued < done + kTeamSlots) {
-    const uint32_t j = pr.issued;
-    const uint32_t P0 = __shfl_sync(0xFFFFFFFFu, bP, j), P1 = __shfl_sync(0xFFFFFFFFu, bP, j + 1);
-    const uint32_t S0 = __shfl_sync(0xFFFFFFFFu, bS, j), S1 = __shfl_sync(0xFFFFFFFFu, bS, j + 1);
-    uint32_t fit = 1;
+  for (;;) {
+    // consumed super-iterations: `empty` phases already complete
+    uint32_t adv = 0;
     if (lane == 0) {
-      const uintptr_t gp0 = reinterpret_cast<uintptr_t>(page + P0) & ~uintptr_t(15);
-      const uintptr_t gp1 = (reinterpret_cast<uintptr_t>(page + P1) + 15) & ~uintptr_t(15);
-      const uintptr_t gs0 = reinterpret_cast<uintptr_t>(ba + S0) & ~uintptr_t(15);
-      const uintptr_t gs1 = (reinterpret_cast<uintptr_t>(ba + S1) + 15) & ~uintptr_t(15);
-      const uint32_t lenp = P1 > P0 ? (uint32_t)(gp1 - gp0) : 0u;
-      uint32_t lens = S1 > S0 ? (uint32_t)(gs1 - gs0) : 0u;
-      const bool pskip = lens > kTeamPs;
-      if (pskip) lens = 0;
-      uint32_t tp = 0xFFFFFFFFu, ts = 0xFFFFFFFFu;
-      if (j != done) {  // oldest unconsumed super-iteration: `done`
-        const uint2 al = lds64(sb + LY::kAlloc + 8u * ((git0 + done) % kTeamSlots));
-        tp = al.x;
-        ts = al.y;
-      } else {
-        pr.pk_head = pr.ps_head = 0;
-      }
-      const uint32_t op = team_place(pr.pk_head, tp, lenp, kTeamPk);
-      const uint32_t ops = team_place(pr.ps_head, ts, lens, kTeamPs);
-      if (op == 0xFFFFFFFFu || ops == 0xFFFFFFFFu) {
-        fit = 0;
-      } else {
-        const uint32_t slot = (git0 + j) % kTeamSlots;
-        const uint32_t bar = sb + LY::kBar + 8u * slot;
-        const uint32_t nrec = min(kTeamSI, nb - j * kTeamSI);
-        const uint32_t pkrel =
-            sb + LY::kPk + op - (uint32_t)(gp0 - reinterpret_cast<uintptr_t>(page));
-        const uint32_t psrel =
-            pskip ? 0u : sb + LY::kPs + ops - (uint32_t)(gs0 - reinterpret_cast<uintptr_t>(ba));
-        sts64(sb + LY::kInfo + 8u * slot, pkrel, psrel);
-        sts64(sb + LY::kAlloc + 8u * slot, op, ops);
-        fence_proxy_async_smem();  // earlier generic reads of the buffers, then async writes
-        mbar_arrive_expect_tx_s(bar, lenp + lens + 16u * nrec);
-        if (lenp)
-          bulk_g2s_s(sb + LY::kPk + op, reinterpret_cast<const void*>(gp0), lenp, bar, pr.policy);
-        bulk_g2s_s(sb + LY::kRec + slot * (kTeamSI * 16u), rec + j * kTeamSI, 16u * nrec, bar,
-                   pr.policy);
-        if (lens)
-          bulk_g2s_s(sb + LY::kPs + ops, reinterpret_cast<const void*>(gs0), lens, bar, pr.policy);
-        pr.pk_head = op + lenp;
-        pr.ps_head = ops + lens;
+      while (pr.done + adv < pr.issued) {
+        const uint32_t g = git0 + pr.done + adv;
+        if (!mbar_test_s(sb + LY::kEmpty + 8u * (g % kTeamSlots), (g / kTeamSlots) & 1u)) break;
+        ++adv;
       }
     }
-    fit = __shfl_sync(0xFFFFFFFFu, fit, 0);
-    if (!fit) break;
-    ++pr.issued;
+    pr.done += __shfl_sync(0xFFFFFFFFu, adv, 0);
+    while (pr.issued < K && pr.issued < pr.done + kTeamSlots) {
+      const uint32_t j = pr.issued;
+      const uint32_t P0 = __shfl_sync(0xFFFFFFFFu, bP, j), P1 = __shfl_sync(0xFFFFFFFFu, bP, j + 1);
+      const uint32_t S0 = __shfl_sync(0xFFFFFFFFu, bS, j), S1 = __shfl_sync(0xFFFFFFFFu, bS, j + 1);
+      uint32_t fit = 1;
+      if (lane == 0) {
+        const uintptr_t gp0 = reinterpret_cast<uintptr_t>(page + P0) & ~uintptr_t(15);
+        const uintptr_t gp1 = (reinterpret_cast<uintptr_t>(page + P1) + 15) & ~uintptr_t(15);
+        const uintptr_t gs0 = reinterpret_cast<uintptr_t>(ba + S0) & ~uintptr_t(15);
+        const uintptr_t gs1 = (reinterpret_cast<uintptr_t>(ba + S1) + 15) & ~uintptr_t(15);
+        const uint32_t lenp = P1 > P0 ? (uint32_t)(gp1 - gp0) : 0u;
+        uint32_t lens = S1 > S0 ? (uint32_t)(gs1 - gs0) : 0u;
+        const bool pskip = lens > kTeamPs;
+        if (pskip) lens = 0;
+        uint32_t tp = 0xFFFFFFFFu, ts = 0xFFFFFFFFu;
+        if (j != pr.done) {  // oldest unconsumed super-iteration: `done`
+          const uint2 al = lds64(sb + LY::kAlloc + 8u * ((git0 + pr.done) % kTeamSlots));
+          tp = al.x;
+          ts = al.y;
+        } else {
+          pr.pk_head = pr.ps_head = 0;
+        }
+        const uint32_t op = team_place(pr.pk_head, tp, lenp, kTeamPk);
+        const uint32_t ops = team_place(pr.ps_head, ts, lens, kTeamPs);
+        if (op == 0xFFFFFFFFu || ops == 0xFFFFFFFFu) {
+          fit = 0;
+        } else {
+          const uint32_t slot = (git0 + j) % kTeamSlots;
+          const uint32_t bar = sb + LY::kBar + 8u * slot;
+          const uint32_t nrec = min(kTeamSI, nb - j * kTeamSI);
+          const uint32_t pkrel =
+              sb + LY::kPk + op - (uint32_t)(gp0 - reinterpret_cast<uintptr_t>(page));
+          const uint32_t psrel =
+              pskip ? 0u : sb + LY::kPs + ops - (uint32_t)(gs0 - reinterpret_cast<uintptr_t>(ba));
+          sts64(sb + LY::kInfo + 8u * slot, pkrel, psrel);
+          sts64(sb + LY::kAlloc + 8u * slot, op, ops);
+          fence_proxy_async_smem();  // earlier generic reads of the buffers, then async writes
+          mbar_arrive_expect_tx_s(bar, lenp + lens + 16u * nrec);
+          if (lenp)
+            bulk_g2s_s(sb + LY::kPk + op, reinterpret_cast<const void*>(gp0), lenp, bar, pr.policy);
+          bulk_g2s_s(sb + LY::kRec + slot * (kTeamSI * 16u), rec + j * kTeamSI, 16u * nrec, bar,
+                     pr.policy);
+          if (lens)
+            bulk_g2s_s(sb + LY::kPs + ops, reinterpret_cast<const void*>(gs0), lens, bar, pr.policy);
+          pr.pk_head = op + lenp;
+          pr.ps_head = ops + lens;
+        }
+      }
+      fit = __shfl_sync(0xFFFFFFFFu, fit, 0);
+      if (!fit) break;
+      ++pr.issued;
+    }
+    if (pr.issued > need || pr.issued >= K) return;
+    // `need` does not fit yet: wait until the oldest staged one is consumed
+    const uint32_t g = git0 + pr.done;
+    mbar_wait_s(sb + LY::kEmpty + 8u * (g % kTeamSlots), (g / kTeamSlots) & 1u);
+    ++pr.done;
   }
 }
 
 template <int DELTA>
-__global__ void __launch_bounds__(kTeamWarps * 32, IZG_TEAM_MINCTAS)
+__global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
     fp_team_kernel(const uint32_t* __restrict__ words, const izg_chunk* __restrict__ chunks,
                    uint32_t n_chunks, uint32_t* __restrict__ out, int32_t* __restrict__ status,
                    uint32_t* __restrict__ consumed, uint32_t* __restrict__ next_chunk,
@@ -424,19 +478,24 @@ __global__ void __launch_bounds__(kTeamWarps * 32, IZG_TEAM_MINCTAS)
   const uint32_t q = lane >> 3, s8 = lane & 7;
   uint32_t sb = smem_u32(smem);
   asm volatile("mov.u32 %0, %0;" : "+r"(sb));  // one register, never rematerialised
-  TeamTile tile;
-  tile.init(sb + LY::kTiles + warp * kStageOut, lane, &omap);
+  TeamTile tile;  // decoding warps only
+  tile.init(sb + LY::kTiles + (warp & (kTeamWarps - 1)) * kStageOut, lane, &omap);
   if (tid == 0) {
-    for (uint32_t i = 0; i < kTeamSlots; ++i) mbar_init_s(sb + LY::kBar + 8u * i, 1);
+    for (uint32_t i = 0; i < kTeamSlots; ++i) {
+      mbar_init_s(sb + LY::kBar + 8u * i, 1);
+      mbar_init_s(sb + LY::kEmpty + 8u * i, kTeamWarps);
+    }
+    for (uint32_t i = 0; i < kTeamWarps; ++i) mbar_init_s(sb + LY::kMbx + 8u * i, 1);
     fence_barrier_init();
   }
   TeamProducer pr;
   pr.policy = policy_evict_first();
-  pr.issued = pr.pk_head = pr.ps_head = 0;
+  pr.issued = pr.done = pr.pk_head = pr.ps_head = 0;
   uint32_t git = 0;  // super-iterations consumed so far, all pages (slot and parity)
   volatile uint32_t* s_page = reinterpret_cast<volatile uint32_t*>(smem + LY::kPage);
 
   for (;;) {
+    TEAM_PROF_T(pt0);
     if (tid == 0) {
       s_page[0] = atomicAdd(next_chunk, 1u);
       s_page[1] = 0;  // a position >= 128 was met
@@ -489,13 +548,31 @@ __global__ void __launch_bounds__(kTeamWarps * 32, IZG_TEAM_MINCTAS)
             sts32(sb + LY::kXrel, 0);
           }
         }
-        if (!ovf)
+        if (!ovf && tid < 256)
           sts32(sb + LY::kSnap + 4u * tid,
                 reinterpret_cast<const uint32_t*>(ix.snap + (size_t)c * 512)[tid]);
         const uint32_t git0 = git;
-        pr.issued = 0;
-        if (warp == 0) team_produce(pr, sb, git0, 0, K, nb, bP, bS, page, ba, rec, lane);
+        if (kArray && tid == 0) {  // the page's initial carry, posted to warp 0's mailbox
+          sts128(sb + LY::kTot, 0, 0, 0, 0);
+          mbar_arrive_s(sb + LY::kMbx);
+        }
         __syncthreads();
+        TEAM_PROF_T(pt1);
+#ifdef IZG_TEAM_PROF
+        long long pwin = 0, pfull = 0, pmbx = 0, pt2 = 0;
+#endif
+        if (warp == kTeamWarps) {
+          // ---- staging warp: every super-iteration of the page, as space frees up
+          pr.issued = pr.done = 0;
+          while (pr.issued < K)
+            team_produce(pr, sb, git0, pr.issued, K, nb, bP, bS, page, ba, rec, lane);
+          while (pr.done < K) {  // observe every `empty` phase (keeps the parities in step)
+            const uint32_t g = git0 + pr.done;
+            mbar_wait_s(sb + LY::kEmpty + 8u * (g % kTeamSlots), (g / kTeamSlots) & 1u);
+            ++pr.done;
+          }
+          git += K;
+        } else {
 
         uint32_t win_end = 0;  // super-iteration at which the next exception window starts
         bool xfast = false;    // this window's highs are unpacked in shared memory
@@ -503,7 +580,9 @@ __global__ void __launch_bounds__(kTeamWarps * 32, IZG_TEAM_MINCTAS)
 #pragma unroll 1
         for (uint32_t k = 0; k < K; ++k, ++git) {
           // ---- exception window --------------------------------------------
+          TEAM_PROF_T(pw0);
           if (k == win_end) {
+            if (k) named_bar_sync(1, kTeamWarps * 32);  // every warp is done with the previous window's highs
             // lane <-> width lane + 1; lo / hi = its cursor at the window's ends
             const uint32_t lo = (k && !ovf) ? lds16(sb + LY::kSnap + 2u * ((k - 1) * 32 + lane)) : 0u;
             uint32_t m = K - k, g = 0, G = 0;
@@ -562,12 +641,16 @@ __global__ void __launch_bounds__(kTeamWarps * 32, IZG_TEAM_MINCTAS)
                        funnel_r(a.w, b.w, sh) & mask);
               }
             }
-            __syncthreads();  // the window's highs and xrel are in place
+            named_bar_sync(1, kTeamWarps * 32);  // the window's highs and xrel are in place
           }
 
           // ---- this warp's four blocks ---------------------------------------
           const uint32_t slot = git % kTeamSlots;
+          TEAM_PROF_T(pw1);
           mbar_wait_s(sb + LY::kBar + 8u * slot, (git / kTeamSlots) & 1u);
+#ifdef IZG_TEAM_PROF
+          { const long long now = clock64(); pwin += pw1 - pw0; pfull += now - pw1; if (k == 0) pt2 = now; }
+#endif
           const uint2 info = lds64(sb + LY::kInfo + 8u * slot);
           const uint32_t blk0 = k * kTeamSI + 4u * warp;
           const bool live = blk0 + q < nb;
@@ -596,35 +679,31 @@ __global__ void __launch_bounds__(kTeamWarps * 32, IZG_TEAM_MINCTAS)
             __syncwarp();
             tile.read(v);
           }
-          uint4 ex = make_uint4(0, 0, 0, 0), incl = ex;
-          uint32_t q3[4] = {0, 0, 0, 0};
+          __syncwarp();
+          if (lane == 0) mbar_arrive_s(sb + LY::kEmpty + 8u * slot);  // done with the staging
           if (kArray) {
+            uint4 ex, incl;
+            uint32_t q3[4] = {0, 0, 0, 0};
             team_scan_local<DELTA>(v, ex, incl, q3, lane);
-            if (lane == 31)
-              sts128(sb + LY::kTot + ((k & 1u) * kTeamWarps + warp) * 16u, incl.x, incl.y, incl.z,
-                     incl.w);
-          }
-          __syncthreads();  // totals out; every warp is done with this slot's staging
-          if (warp == 0) team_produce(pr, sb, git0, k + 1, K, nb, bP, bS, page, ba, rec, lane);
-          if (kArray) {
-            // entry l of the totals: warp l / 4, component l % 4
-            uint32_t x = lds32(sb + LY::kTot + (k & 1u) * kTeamWarps * 16u + 4u * lane);
-            shfl_up_add(x, 4);
-            shfl_up_add(x, 8);
-            shfl_up_add(x, 16);
-            const int src = (4 * (warp - 1)) & 31;
-            uint4 pre, all;
-            pre.x = __shfl_sync(0xFFFFFFFFu, x, src);
-            pre.y = NC > 1 ? __shfl_sync(0xFFFFFFFFu, x, src + 1) : 0u;
-            pre.z = NC > 2 ? __shfl_sync(0xFFFFFFFFu, x, src + 2) : 0u;
-            pre.w = NC > 2 ? __shfl_sync(0xFFFFFFFFu, x, src + 3) : 0u;
-            if (warp == 0) pre = make_uint4(0, 0, 0, 0);
-            all.x = __shfl_sync(0xFFFFFFFFu, x, 28);
-            all.y = NC > 1 ? __shfl_sync(0xFFFFFFFFu, x, 29) : 0u;
-            all.z = NC > 2 ? __shfl_sync(0xFFFFFFFFu, x, 30) : 0u;
-            all.w = NC > 2 ? __shfl_sync(0xFFFFFFFFu, x, 31) : 0u;
-            team_scan_apply<DELTA>(v, u4add(u4add(carry, pre), ex), q3);
-            carry = u4add(carry, all);
+            // carry chain: the prefix up to the previous warp iteration arrives
+            // in this warp's mailbox; post ours to the next warp's
+#ifndef IZG_ABL_TEAM_NOCHAIN  // developer ablation (wrong output): no wait on the carry chain
+            TEAM_PROF_T(pm0);
+            mbar_wait_s(sb + LY::kMbx + 8u * warp, git & 1u);
+#ifdef IZG_TEAM_PROF
+            pmbx += clock64() - pm0;
+#endif
+#endif
+            const uint4 pv = lds128(sb + LY::kTot + 16u * warp);
+            __syncwarp();  // everyone has read the mailbox before the chain can refill it
+            if (lane == 31) {
+              const bool last = warp == kTeamWarps - 1;
+              const uint32_t dst = last ? (k + 1 == K ? kTeamWarps : 0) : warp + 1;
+              sts128(sb + LY::kTot + 16u * dst, pv.x + incl.x, pv.y + incl.y, pv.z + incl.z,
+                     pv.w + incl.w);
+              if (dst != kTeamWarps) mbar_arrive_s(sb + LY::kMbx + 8u * dst);
+            }
+            team_scan_apply<DELTA>(v, u4add(pv, ex), q3);
           }
           if (orow >= 0 && blk0 + 4 <= nb) {
             if (!tot) tile.wait_free();
@@ -636,12 +715,27 @@ __global__ void __launch_bounds__(kTeamWarps * 32, IZG_TEAM_MINCTAS)
           }
         }
         if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) s_page[1] = 1;
+#ifdef IZG_TEAM_PROF
+        if (tid == 0) {
+          const long long pt3 = clock64();
+          TEAM_PROF_ADD(0, 1); TEAM_PROF_ADD(1, pt1 - pt0); TEAM_PROF_ADD(2, pt2 - pt1);
+          TEAM_PROF_ADD(3, pwin); TEAM_PROF_ADD(4, pt3 - pt2); TEAM_PROF_ADD(6, pfull);
+          TEAM_PROF_ADD(7, pmbx);
+          s_page[2] = (uint32_t)pt3;
+        }
+#endif
+        }  // decoding warps
         pos = h.z;
       }
     }
-    __syncthreads();  // bad flag; s_page[0] read by everyone before the next claim
-    if (decoded && s_page[1]) st = IZG_E_FP_POS_RANGE;
+    __syncthreads();  // bad flag, final carry; s_page[0] read by everyone before the next claim
+#ifdef IZG_TEAM_PROF
+    if (tid == 0 && decoded) TEAM_PROF_ADD(5, (uint32_t)((uint32_t)clock64() - s_page[2]));
+#endif
     if (warp == 0) {
+      if (decoded && s_page[1]) st = IZG_E_FP_POS_RANGE;
+      if (decoded && kArray) carry = lds128(sb + LY::kTot + 16u * kTeamWarps);
+      __syncwarp();
       if (kArray && st == IZG_OK) {
         if (core < ch.n) {  // Variable Byte remainder (codec.cpp:56-62)
           uint32_t rb = 0;
@@ -660,7 +754,7 @@ __global__ void __launch_bounds__(kTeamWarps * 32, IZG_TEAM_MINCTAS)
       }
     }
   }
-  tile.drain();
+  if (warp < kTeamWarps) tile.drain();
 }
 
 }  // namespace izg
