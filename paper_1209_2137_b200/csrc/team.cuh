@@ -44,15 +44,14 @@ constexpr int kTeamWarps = 8;
 constexpr uint32_t kTeamSI = 4 * kTeamWarps;  // blocks per super-iteration
 constexpr uint32_t kTeamSlots = 4;            // super-iterations staged ahead
 #ifndef IZG_TEAM_PK
-#define IZG_TEAM_PK (20 * 1024)
+#define IZG_TEAM_PK 16896
 #endif
 #ifndef IZG_TEAM_XB
-#define IZG_TEAM_XB (16 * 1024)
+#define IZG_TEAM_XB 8192  // per window; two windows (one in use, one being staged)
 #endif
 constexpr uint32_t kTeamPk = IZG_TEAM_PK;     // packed words staging (>= 16 KiB + 16)
 constexpr uint32_t kTeamPs = 5 * 1024;        // position bytes staging
-constexpr uint32_t kTeamXb = IZG_TEAM_XB;     // unpacked exception highs of a window
-constexpr uint32_t kTeamXGroups = kTeamXb / 512;
+constexpr uint32_t kTeamXb = IZG_TEAM_XB;     // packed exception arrays of a window
 #ifndef IZG_TEAM_UNPACK
 #define IZG_TEAM_UNPACK team_unpack_window  // or team_unpack_rows (more row loads, fewer moves)
 #endif
@@ -66,9 +65,9 @@ constexpr int kTeamThreads = (kTeamWarps + 1) * 32;  // 8 decoding warps + the s
 #define IZG_TEAM_LB_THREADS ((kTeamWarps + 1) * 32)
 
 #ifdef IZG_TEAM_PROF  // developer build: where a page's time goes (cycles, summed over pages)
-// [0] pages, [1] claim -> setup barrier, [2] setup barrier -> first staging landed (warp 0),
-// [3] window set-ups (warp 0, incl. barriers), [4] iterations (warp 0), [5] loop end -> page end
-// [6] warp 0: waits on `full`, [7] warp 0: waits on the carry mailbox
+// decoding warp 0, cycles: [0] pages, [1] waits for a page descriptor, [2] for an exception
+// window, [3] for staged data, [4] for the carry mailbox, [5] whole pages; staging warp:
+// [6] passes without progress
 __device__ unsigned long long g_team_prof[8];
 #define TEAM_PROF_T(x) const long long x = clock64()
 #define TEAM_PROF_ADD(i, v) atomicAdd(&g_team_prof[i], (unsigned long long)(v))
@@ -78,24 +77,38 @@ __device__ unsigned long long g_team_prof[8];
 #endif
 
 struct TeamLayout {
-  static constexpr uint32_t kTiles = 0;  // one 2 KiB output tile per warp (1024-aligned)
-  static constexpr uint32_t kPk = kTiles + kTeamWarps * kStageOut;
-  static constexpr uint32_t kPs = kPk + kTeamPk;
-  static constexpr uint32_t kRec = kPs + kTeamPs;
-  static constexpr uint32_t kXb = kRec + kTeamSlots * kTeamSI * 16;
-  static constexpr uint32_t kSnap = kXb + kTeamXb;       // u16 [16][32]
-  static constexpr uint32_t kXrel = kSnap + 1024;        // i32 [36]
-  static constexpr uint32_t kDirb = kXrel + 36 * 4;      // u32 [36]
-  static constexpr uint32_t kTot = kDirb + 36 * 4;       // uint4 [warps + 1]: carry mailboxes, final carry
-  static constexpr uint32_t kInfo = kTot + (kTeamWarps + 1) * 16;  // uint2 [slots] {pkrel, psrel}
-  static constexpr uint32_t kAlloc = kInfo + kTeamSlots * 8;     // uint2 [slots] {pk off, ps off}
-  static constexpr uint32_t kBar = kAlloc + kTeamSlots * 8;      // u64 [slots]: staging landed
-  static constexpr uint32_t kEmpty = kBar + kTeamSlots * 8;      // u64 [slots]: staging read by all warps
-  static constexpr uint32_t kMbx = kEmpty + kTeamSlots * 8;      // u64 [warps]: mailbox posted
-  static constexpr uint32_t kPage = kMbx + kTeamWarps * 8;       // u32 page, u32 bad flag
-  static constexpr size_t kSmem = kPage + 16;
+  static constexpr uint32_t kTiles = 0;  // one 2 KiB output tile per decoding warp (1024-aligned)
+  static constexpr uint32_t kPk = kTiles + kTeamWarps * kStageOut;  // packed words staging
+  static constexpr uint32_t kPs = kPk + kTeamPk;                    // position bytes staging
+  static constexpr uint32_t kRec = kPs + kTeamPs;                   // block records [slots][32]
+  static constexpr uint32_t kXb = kRec + kTeamSlots * kTeamSI * 16; // exception highs, two windows
+  // staging warp's page contexts [2]: bounds P[20], S[20], array bases [32], scalars [24],
+  // cursor snapshots u16 [16][32]
+  static constexpr uint32_t kCtxBytes = (20 + 20 + 32 + 24) * 4 + 1024;
+  static constexpr uint32_t kCtx = kXb + 2 * kTeamXb;
+  // per window, per width: {shared address of the first staged group, its first value's index}
+  static constexpr uint32_t kXrel = kCtx + 2 * kCtxBytes;  // uint2 [2][36]
+  static constexpr uint32_t kDirb = kXrel + 2 * 36 * 8;   // u32 [2][36]: per page, array base word
+  static constexpr uint32_t kTot = kDirb + 2 * 36 * 4;    // uint4 [warps]: carry mailboxes
+  static constexpr uint32_t kDesc = kTot + kTeamWarps * 16;        // u32 [2][16]: page descriptors
+  static constexpr uint32_t kXinfo = kDesc + 2 * 64;               // uint2 [2] {window end, fast}
+  static constexpr uint32_t kInfo = kXinfo + 2 * 8;                // uint2 [slots] {pkrel, psrel}
+  static constexpr uint32_t kAlloc = kInfo + kTeamSlots * 8;       // uint2 [slots] {pk off, ps off}
+  static constexpr uint32_t kBar = kAlloc + kTeamSlots * 8;        // u64 [slots]: staging landed
+  static constexpr uint32_t kEmpty = kBar + kTeamSlots * 8;        // u64 [slots]: staging read by all warps
+  static constexpr uint32_t kMbx = kEmpty + kTeamSlots * 8;        // u64 [warps]: mailbox posted
+  static constexpr uint32_t kXfull = kMbx + kTeamWarps * 8;        // u64 [2]: window prepared
+  static constexpr uint32_t kXempty = kXfull + 16;                 // u64 [2]: window consumed
+  static constexpr uint32_t kPfull = kXempty + 16;                 // u64 [2]: descriptor written
+  static constexpr uint32_t kPdone = kPfull + 16;                  // u64 [2]: warps 0..6 left the page
+  static constexpr uint32_t kPfree = kPdone + 16;                  // u64 [2]: page finished
+  static constexpr uint32_t kBad = kPfree + 16;                    // u32 [2]: a position >= 128 was met
+  static constexpr size_t kSmem = kBad + 16;
 };
-static_assert(TeamLayout::kXrel % 16 == 0 && TeamLayout::kTot % 16 == 0, "team layout");
+static_assert(TeamLayout::kXrel % 16 == 0 && TeamLayout::kTot % 16 == 0 &&
+                  TeamLayout::kDesc % 16 == 0 && TeamLayout::kBar % 8 == 0,
+              "team layout");
+static_assert(IZG_TEAM_MINCTAS * (TeamLayout::kSmem + 1024) <= 228 * 1024, "team shared memory");
 static_assert(kTeamPk >= 16384 + 16 && kTeamPk % 16 == 0 && kTeamPs % 16 == 0, "team staging");
 
 // Linear staging: unpack_slots_aligned's "ring" without a wrap.
@@ -231,33 +244,42 @@ __device__ __forceinline__ void team_unpack_words(uint32_t bw, uint32_t width, u
 
 // Patch one warp iteration from shared memory: lanes 8q..8q+7 patch block q,
 // sixteen exceptions per round.  `ps` = shared address of the block's first
-// position byte, `xa` = shared address of its first exception high.
-__device__ __forceinline__ bool team_patch(uint32_t t, uint32_t ps, uint32_t xa, uint32_t myb,
-                                           uint32_t myc, int lane) {
+// position byte; the block's width-w array is staged packed (vertical
+// groups of 128, codec_patched.cpp:346-379) from shared address `xa`, and
+// its exceptions are values rc, rc + 1, ... counted from the first staged
+// group: value r lies in group r / 128, lane r % 4, slot (r % 128) / 4.
+__device__ __forceinline__ bool team_patch(uint32_t t, uint32_t ps, uint32_t xa, uint32_t rc,
+                                           uint32_t myw, uint32_t myb, uint32_t myc, int lane) {
   const uint32_t q = (lane >> 3) & 3u, s8 = lane & 7;
   uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));
   mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));
   // integer p of block q: tile byte 512 q + (4 p ^ 16 ((row & 7))), row = 4 q + p / 32,
   // i.e. (t + 512 q) ^ 64 (q & 1) ^ (4 p) ^ 16 (p / 32)
   const uint32_t tqr = (t + (q << 9)) ^ ((q & 1u) << 6);
+  const uint32_t wmask = low_mask(myw), w16 = 16u * myw;
   uint32_t badp = 0;
   for (uint32_t e0 = s8; e0 < mxc; e0 += 16) {
-    uint32_t pp[2], xv[2];
+    uint32_t pp[2], lo[2], hi[2], sh[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const uint32_t e = e0 + 8u * j;
       pp[j] = 0x100u;  // idle slot: no patch, not a position error
-      xv[j] = 0;
+      lo[j] = hi[j] = sh[j] = 0;
       if (e < myc) {
+        const uint32_t r = rc + e, tt = r & 127u, bit = (tt >> 2) * myw;
+        const uint32_t a = xa + (r >> 7) * w16 + ((bit >> 5) << 4) + ((tt & 3u) << 2);
+        sh[j] = bit & 31u;
         pp[j] = lds8(ps + e);
-        xv[j] = lds32(xa + 4u * e);
+        lo[j] = lds32(a);
+        hi[j] = lds32(a + 16u);
       }
     }
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const uint32_t p = pp[j];
       const uint32_t a = tqr ^ (((p >> 1) & 0x30u) ^ (p << 2));
-      if (p < 128u) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(xv[j] << myb) : "memory");
+      const uint32_t hv = (funnel_r(lo[j], hi[j], sh[j]) & wmask) << myb;
+      if (p < 128u) asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(hv) : "memory");
       badp |= p;  // bit 7: a position in 128..255 (codec_patched.cpp:328-330)
     }
   }
@@ -342,10 +364,9 @@ __device__ __forceinline__ void team_scan_apply(uint32_t (&v)[4][4], const uint4
   }
 }
 
-// Producer state of a page (warp 0; lane 0 issues the copies).
+// Staging state (the staging warp; lane 0 allocates and issues the copies).
 struct TeamProducer {
-  uint32_t issued;            // super-iterations of this page staged so far
-  uint32_t done;              // super-iterations every warp has finished reading
+  uint32_t gi, gd;            // super-iterations staged / read by every warp (all pages)
   uint32_t pk_head, ps_head;  // allocation heads of the two staging buffers
   uint64_t policy;
 };
@@ -378,89 +399,81 @@ __device__ __forceinline__ uint32_t team_place(uint32_t head, uint32_t tail, uin
   return head + len <= tail ? head : 0xFFFFFFFFu;
 }
 
-// Stage super-iterations until number `need` is staged, and beyond it while
-// they fit, up to kTeamSlots past the `done` consumed ones.  All lanes of
-// warp 0 call (the bounds live in lanes 0..16); lane 0 allocates and issues.
-// A super-iteration counts as consumed once every warp has arrived on its
-// slot's `empty` barrier.  Per super-iteration j: the packed words
+// Stage super-iteration j of a page (global number pr.gi) if its data fit
+// the staging buffers next to what is still unread: the packed words
 // [P_j, P_j+1), its block records, and the byte-array bytes [S_j, S_j+1)
 // (skipped when they exceed the buffer: that super-iteration patches from
 // global memory), each as the 16-byte-aligned span covering it, all
 // completing on the slot's `full` barrier.  info[slot] = {shared address of
 // page word 0, shared address of byte-array byte 0 (0: not staged)}.
-__device__ __forceinline__ void team_produce(TeamProducer& pr, uint32_t sb, uint32_t git0,
-                                             uint32_t need, uint32_t K, uint32_t nb, uint32_t bP,
-                                             uint32_t bS, const uint32_t* page, const uint8_t* ba,
-                                             const uint4* rec, int lane) {
+// `ctx` = the page's context (bounds P at +0, S at +80).  Lane 0 only.
+__device__ __forceinline__ bool team_issue(TeamProducer& pr, uint32_t sb, uint32_t ctx, uint32_t j,
+                                           uint32_t nb, const uint32_t* page, const uint8_t* ba,
+                                           const uint4* rec) {
   using LY = TeamLayout;
-  for (;;) {
-    // consumed super-iterations: `empty` phases already complete
-    uint32_t adv = 0;
-    if (lane == 0) {
-      while (pr.done + adv < pr.issued) {
-        const uint32_t g = git0 + pr.done + adv;
-        if (!mbar_test_s(sb + LY::kEmpty + 8u * (g % kTeamSlots), (g / kTeamSlots) & 1u)) break;
-        ++adv;
-      }
+  const uint32_t P0 = lds32(ctx + 4u * j), P1 = lds32(ctx + 4u * j + 4u);
+  const uint32_t S0 = lds32(ctx + 80u + 4u * j), S1 = lds32(ctx + 84u + 4u * j);
+  const uintptr_t gp0 = reinterpret_cast<uintptr_t>(page + P0) & ~uintptr_t(15);
+  const uintptr_t gp1 = (reinterpret_cast<uintptr_t>(page + P1) + 15) & ~uintptr_t(15);
+  const uintptr_t gs0 = reinterpret_cast<uintptr_t>(ba + S0) & ~uintptr_t(15);
+  const uintptr_t gs1 = (reinterpret_cast<uintptr_t>(ba + S1) + 15) & ~uintptr_t(15);
+  const uint32_t lenp = P1 > P0 ? (uint32_t)(gp1 - gp0) : 0u;
+  uint32_t lens = S1 > S0 ? (uint32_t)(gs1 - gs0) : 0u;
+  const bool pskip = lens > kTeamPs;
+  if (pskip) lens = 0;
+  uint32_t tp = 0xFFFFFFFFu, ts = 0xFFFFFFFFu;
+  if (pr.gi != pr.gd) {  // oldest unread super-iteration: gd
+    const uint2 al = lds64(sb + LY::kAlloc + 8u * (pr.gd % kTeamSlots));
+    tp = al.x;
+    ts = al.y;
+  } else {
+    pr.pk_head = pr.ps_head = 0;
+  }
+  const uint32_t op = team_place(pr.pk_head, tp, lenp, kTeamPk);
+  const uint32_t ops = team_place(pr.ps_head, ts, lens, kTeamPs);
+  if (op == 0xFFFFFFFFu || ops == 0xFFFFFFFFu) return false;
+  const uint32_t slot = pr.gi % kTeamSlots;
+  const uint32_t bar = sb + LY::kBar + 8u * slot;
+  const uint32_t nrec = min(kTeamSI, nb - j * kTeamSI);
+  const uint32_t pkrel = sb + LY::kPk + op - (uint32_t)(gp0 - reinterpret_cast<uintptr_t>(page));
+  const uint32_t psrel =
+      pskip ? 0u : sb + LY::kPs + ops - (uint32_t)(gs0 - reinterpret_cast<uintptr_t>(ba));
+  sts64(sb + LY::kInfo + 8u * slot, pkrel, psrel);
+  sts64(sb + LY::kAlloc + 8u * slot, op, ops);
+  fence_proxy_async_smem();  // earlier generic reads of the buffers, then async writes
+  mbar_arrive_expect_tx_s(bar, lenp + lens + 16u * nrec);
+  if (lenp) bulk_g2s_s(sb + LY::kPk + op, reinterpret_cast<const void*>(gp0), lenp, bar, pr.policy);
+  bulk_g2s_s(sb + LY::kRec + slot * (kTeamSI * 16u), rec + j * kTeamSI, 16u * nrec, bar, pr.policy);
+  if (lens) bulk_g2s_s(sb + LY::kPs + ops, reinterpret_cast<const void*>(gs0), lens, bar, pr.policy);
+  pr.pk_head = op + lenp;
+  pr.ps_head = ops + lens;
+  return true;
+}
+
+// End of a chunk (one warp): VByte remainder (codec.cpp:56-62), exact
+// consumption (codec.cpp:63-64), status and words consumed.
+template <int DELTA>
+__device__ __forceinline__ void team_finish(int32_t st, uint32_t pos, uint4 carry,
+                                            const izg_chunk& ch, const uint32_t* page, uint32_t* o,
+                                            uint32_t c, int32_t* status, uint32_t* consumed,
+                                            int lane) {
+  constexpr bool kArray = DELTA != IZG_DELTA_NONE;
+  if (kArray && st == IZG_OK) {
+    const uint32_t core = ch.n / 128 * 128;
+    if (core < ch.n) {
+      uint32_t rb = 0;
+      if (lane == 0)
+        st = vbyte_tail<DELTA>(reinterpret_cast<const uint8_t*>(page + pos), 4u * (ch.n_words - pos),
+                               core, ch.n - core, carry, o, &rb);
+      st = __shfl_sync(0xFFFFFFFFu, st, 0);
+      rb = __shfl_sync(0xFFFFFFFFu, rb, 0);
+      if (st == IZG_OK) pos += (rb + 3) / 4;
     }
-    pr.done += __shfl_sync(0xFFFFFFFFu, adv, 0);
-    while (pr.issued < K && pr.issued < pr.done + kTeamSlots) {
-      const uint32_t j = pr.issued;
-      const uint32_t P0 = __shfl_sync(0xFFFFFFFFu, bP, j), P1 = __shfl_sync(0xFFFFFFFFu, bP, j + 1);
-      const uint32_t S0 = __shfl_sync(0xFFFFFFFFu, bS, j), S1 = __shfl_sync(0xFFFFFFFFu, bS, j + 1);
-      uint32_t fit = 1;
-      if (lane == 0) {
-        const uintptr_t gp0 = reinterpret_cast<uintptr_t>(page + P0) & ~uintptr_t(15);
-        const uintptr_t gp1 = (reinterpret_cast<uintptr_t>(page + P1) + 15) & ~uintptr_t(15);
-        const uintptr_t gs0 = reinterpret_cast<uintptr_t>(ba + S0) & ~uintptr_t(15);
-        const uintptr_t gs1 = (reinterpret_cast<uintptr_t>(ba + S1) + 15) & ~uintptr_t(15);
-        const uint32_t lenp = P1 > P0 ? (uint32_t)(gp1 - gp0) : 0u;
-        uint32_t lens = S1 > S0 ? (uint32_t)(gs1 - gs0) : 0u;
-        const bool pskip = lens > kTeamPs;
-        if (pskip) lens = 0;
-        uint32_t tp = 0xFFFFFFFFu, ts = 0xFFFFFFFFu;
-        if (j != pr.done) {  // oldest unconsumed super-iteration: `done`
-          const uint2 al = lds64(sb + LY::kAlloc + 8u * ((git0 + pr.done) % kTeamSlots));
-          tp = al.x;
-          ts = al.y;
-        } else {
-          pr.pk_head = pr.ps_head = 0;
-        }
-        const uint32_t op = team_place(pr.pk_head, tp, lenp, kTeamPk);
-        const uint32_t ops = team_place(pr.ps_head, ts, lens, kTeamPs);
-        if (op == 0xFFFFFFFFu || ops == 0xFFFFFFFFu) {
-          fit = 0;
-        } else {
-          const uint32_t slot = (git0 + j) % kTeamSlots;
-          const uint32_t bar = sb + LY::kBar + 8u * slot;
-          const uint32_t nrec = min(kTeamSI, nb - j * kTeamSI);
-          const uint32_t pkrel =
-              sb + LY::kPk + op - (uint32_t)(gp0 - reinterpret_cast<uintptr_t>(page));
-          const uint32_t psrel =
-              pskip ? 0u : sb + LY::kPs + ops - (uint32_t)(gs0 - reinterpret_cast<uintptr_t>(ba));
-          sts64(sb + LY::kInfo + 8u * slot, pkrel, psrel);
-          sts64(sb + LY::kAlloc + 8u * slot, op, ops);
-          fence_proxy_async_smem();  // earlier generic reads of the buffers, then async writes
-          mbar_arrive_expect_tx_s(bar, lenp + lens + 16u * nrec);
-          if (lenp)
-            bulk_g2s_s(sb + LY::kPk + op, reinterpret_cast<const void*>(gp0), lenp, bar, pr.policy);
-          bulk_g2s_s(sb + LY::kRec + slot * (kTeamSI * 16u), rec + j * kTeamSI, 16u * nrec, bar,
-                     pr.policy);
-          if (lens)
-            bulk_g2s_s(sb + LY::kPs + ops, reinterpret_cast<const void*>(gs0), lens, bar, pr.policy);
-          pr.pk_head = op + lenp;
-          pr.ps_head = ops + lens;
-        }
-      }
-      fit = __shfl_sync(0xFFFFFFFFu, fit, 0);
-      if (!fit) break;
-      ++pr.issued;
-    }
-    if (pr.issued > need || pr.issued >= K) return;
-    // `need` does not fit yet: wait until the oldest staged one is consumed
-    const uint32_t g = git0 + pr.done;
-    mbar_wait_s(sb + LY::kEmpty + 8u * (g % kTeamSlots), (g / kTeamSlots) & 1u);
-    ++pr.done;
+    if (st == IZG_OK && pos != ch.n_words) st = IZG_E_PAYLOAD_SIZE;
+  }
+  if (lane == 0) {
+    status[c] = st;
+    if (consumed) consumed[c] = st == IZG_OK ? pos : 0;
   }
 }
 
@@ -473,288 +486,420 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
   extern __shared__ __align__(1024) uint8_t smem[];
   using LY = TeamLayout;
   constexpr bool kArray = DELTA != IZG_DELTA_NONE;
-  constexpr int NC = DELTA == IZG_DELTA_D4 ? 4 : DELTA == IZG_DELTA_D2 ? 2 : 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t q = lane >> 3, s8 = lane & 7;
   uint32_t sb = smem_u32(smem);
   asm volatile("mov.u32 %0, %0;" : "+r"(sb));  // one register, never rematerialised
-  TeamTile tile;  // decoding warps only
-  tile.init(sb + LY::kTiles + (warp & (kTeamWarps - 1)) * kStageOut, lane, &omap);
   if (tid == 0) {
     for (uint32_t i = 0; i < kTeamSlots; ++i) {
       mbar_init_s(sb + LY::kBar + 8u * i, 1);
       mbar_init_s(sb + LY::kEmpty + 8u * i, kTeamWarps);
     }
     for (uint32_t i = 0; i < kTeamWarps; ++i) mbar_init_s(sb + LY::kMbx + 8u * i, 1);
-    fence_barrier_init();
-  }
-  TeamProducer pr;
-  pr.policy = policy_evict_first();
-  pr.issued = pr.done = pr.pk_head = pr.ps_head = 0;
-  uint32_t git = 0;  // super-iterations consumed so far, all pages (slot and parity)
-  volatile uint32_t* s_page = reinterpret_cast<volatile uint32_t*>(smem + LY::kPage);
-
-  for (;;) {
-    TEAM_PROF_T(pt0);
-    if (tid == 0) {
-      s_page[0] = atomicAdd(next_chunk, 1u);
-      s_page[1] = 0;  // a position >= 128 was met
+    for (uint32_t i = 0; i < 2; ++i) {
+      mbar_init_s(sb + LY::kXfull + 8u * i, 1);
+      mbar_init_s(sb + LY::kXempty + 8u * i, kTeamWarps);
+      mbar_init_s(sb + LY::kPfull + 8u * i, 1);
+      mbar_init_s(sb + LY::kPdone + 8u * i, kTeamWarps - 1);
+      mbar_init_s(sb + LY::kPfree + 8u * i, 1);
     }
-    __syncthreads();
-    const uint32_t c = s_page[0];
-    if (c >= n_chunks) break;
-    const izg_chunk ch = chunks[c];
-    int32_t st = precheck(IZG_SIMDFASTPFOR, kArray, ch.n);
-    uint32_t pos = 0;
-    uint4 carry = make_uint4(0, 0, 0, 0);
-    const uint32_t* page = words + ch.word_off;
-    uint32_t* o = out + ch.out_off;
-    const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
-    const uint32_t nb = core / 128;
-    bool decoded = false;
-    if (st == IZG_OK && nb) {
-      const uint4 h = ix.hdr[c];
-      st = (int32_t)(h.x & 0xFFu);
-      const uint4* rec = ix.page_rec(c);
-      if (st) {
-        if (!(st == IZG_E_FP_TRUNC_PAGE || st == IZG_E_FP_BA_OFFSET || st == IZG_E_FP_TRUNC_BA) &&
-            fp_positions_bad_idx(rec, reinterpret_cast<const uint8_t*>(page + h.w + 1),
-                                 (h.x >> 8) & 0xFFFFu, lane))
-          st = IZG_E_FP_POS_RANGE;
-      } else {
-        decoded = true;
-        const uint32_t A = h.w;
-        const bool ovf = (h.x >> 31) != 0;  // a cursor passed 65,535: no snapshots
-        const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
-        const bool oal = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
-        const int64_t orow = tma_out && (ch.out_off & 31) == 0 ? (int64_t)(ch.out_off >> 5) : -1;
-        const bool pal = (reinterpret_cast<uintptr_t>(page + 1) & 15) == 0;  // packed rows aligned
-        const bool xal = (reinterpret_cast<uintptr_t>(page) & 15) == 0;      // exception rows aligned
-        const uint32_t K = (nb + kTeamSI - 1) / kTeamSI;
-        // Super-iteration bounds, lane l <-> boundary l (0..16): packed word
-        // and byte-array offset of block 32 l, or the ends.
-        uint32_t bP = A, bS = 4u * (h.y - A - 1);
-        if ((uint32_t)lane * kTeamSI < nb) {
-          const uint4 e = rec[(uint32_t)lane * kTeamSI];
-          bP = e.y;
-          bS = e.z - 3u;
-        }
-        const uint32_t dirv = ix.dir[(size_t)c * 32 + lane];  // lane <-> width lane + 1
-        if (warp == 0) {
-          sts32(sb + LY::kDirb + 4u * (lane + 1), dirv);
-          sts32(sb + LY::kXrel + 4u * (lane + 1), 0);
+    fence_barrier_init();
+    if (kArray) {  // the first page's initial carry, posted to warp 0's mailbox
+      sts128(sb + LY::kTot, 0, 0, 0, 0);
+      mbar_arrive_s(sb + LY::kMbx);
+    }
+  }
+  __syncthreads();
+
+  if (warp == kTeamWarps) {
+    // ======================= staging warp ====================================
+    // Runs ahead of the decoding warps as two in-order streams over the
+    // pages it claims: (a) staging of super-iterations (TMA), (b) exception
+    // windows (bulk unpack into the free half of xbuf, one batch of groups
+    // per pass), stream (b) up to a page ahead of (a).  Pages that need no
+    // decode (argument errors, index-pass errors, arrays shorter than a
+    // block) are settled here.  Each decodable page gets a context (bounds,
+    // array bases, snapshots; two contexts, by page parity) and a published
+    // descriptor for the decoding warps.
+    TeamProducer pr;
+    pr.policy = policy_evict_first();
+    pr.gi = pr.gd = pr.pk_head = pr.ps_head = 0;
+    auto claim = [&]() -> uint32_t {
+      uint32_t c = 0;
+      if (lane == 0) c = atomicAdd(next_chunk, 1u);
+      c = __shfl_sync(0xFFFFFFFFu, c, 0);
+      if (c < n_chunks) {  // its index records towards L2: read one page later
+        const uint8_t* p = nullptr;
+        if (lane == 0) p = reinterpret_cast<const uint8_t*>(chunks + c);
+        else if (lane == 1) p = reinterpret_cast<const uint8_t*>(ix.hdr + c);
+        else if (lane == 2) p = reinterpret_cast<const uint8_t*>(ix.dir + (size_t)c * 32);
+        else if (lane < 11) p = reinterpret_cast<const uint8_t*>(ix.snap + (size_t)c * 512) + 128 * (lane - 3);
+        else if (lane < 28) p = reinterpret_cast<const uint8_t*>(ix.page_rec(c) + min(32u * (lane - 11), kMaxBlocks - 1));
+        if (p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      }
+      return c;
+    };
+    // context scalars (u32 index from +288): 0 c, 1 nb, 2 K, 3 A, 4 flags (1 ovf, 2 exception rows
+    // aligned), 5..6 word_off
+    constexpr uint32_t kScal = 288, kSnapOff = (20 + 20 + 32 + 24) * 4;
+    uint32_t c_next = claim();
+    uint32_t pprep = 0;   // decodable pages prepared so far (contexts / descriptors written)
+    bool ended = false;   // the END descriptor is out
+    uint32_t pa = 0, ka = 0;    // stream (a): page, next super-iteration to stage
+    uint32_t pb = 0, wkb = 0;   // stream (b): page, first super-iteration without a window
+    uint32_t wprep = 0;         // windows prepared so far
+    for (;;) {
+      bool progress = false;
+      // ---- a new page, when a stream needs one and a context is free ----------
+      if (!ended && (pa == pprep || pb == pprep) && min(pa, pb) + 2 > pprep) {
+        const uint32_t c = c_next;
+        const uint32_t pp = pprep & 1u;
+        if (c >= n_chunks) {  // no more pages: tell the decoding warps
+          if (pprep >= 2) mbar_wait_s(sb + LY::kPfree + 8u * pp, ((pprep >> 1) - 1u) & 1u);
           if (lane == 0) {
-            sts32(sb + LY::kDirb, 0);
-            sts32(sb + LY::kXrel, 0);
+            sts128(sb + LY::kDesc + 64u * pp, 0, 1u, 0, 0);
+            mbar_arrive_s(sb + LY::kPfull + 8u * pp);
           }
-        }
-        if (!ovf && tid < 256)
-          sts32(sb + LY::kSnap + 4u * tid,
-                reinterpret_cast<const uint32_t*>(ix.snap + (size_t)c * 512)[tid]);
-        const uint32_t git0 = git;
-        if (kArray && tid == 0) {  // the page's initial carry, posted to warp 0's mailbox
-          sts128(sb + LY::kTot, 0, 0, 0, 0);
-          mbar_arrive_s(sb + LY::kMbx);
-        }
-        __syncthreads();
-        TEAM_PROF_T(pt1);
-#ifdef IZG_TEAM_PROF
-        long long pwin = 0, pfull = 0, pmbx = 0, pt2 = 0;
-#endif
-        if (warp == kTeamWarps) {
-          // ---- staging warp: every super-iteration of the page, as space frees up
-          pr.issued = pr.done = 0;
-          while (pr.issued < K)
-            team_produce(pr, sb, git0, pr.issued, K, nb, bP, bS, page, ba, rec, lane);
-          while (pr.done < K) {  // observe every `empty` phase (keeps the parities in step)
-            const uint32_t g = git0 + pr.done;
-            mbar_wait_s(sb + LY::kEmpty + 8u * (g % kTeamSlots), (g / kTeamSlots) & 1u);
-            ++pr.done;
-          }
-          git += K;
+          ended = true;
         } else {
-
-        uint32_t win_end = 0;  // super-iteration at which the next exception window starts
-        bool xfast = false;    // this window's highs are unpacked in shared memory
-        bool bad = false;
-#pragma unroll 1
-        for (uint32_t k = 0; k < K; ++k, ++git) {
-          // ---- exception window --------------------------------------------
-          TEAM_PROF_T(pw0);
-          if (k == win_end) {
-            if (k) named_bar_sync(1, kTeamWarps * 32);  // every warp is done with the previous window's highs
-            // lane <-> width lane + 1; lo / hi = its cursor at the window's ends
-            const uint32_t lo = (k && !ovf) ? lds16(sb + LY::kSnap + 2u * ((k - 1) * 32 + lane)) : 0u;
-            uint32_t m = K - k, g = 0, G = 0;
-            xfast = false;
-            if (!ovf) {
-              for (;;) {
-                const uint32_t hi = lds16(sb + LY::kSnap + 2u * ((k + m - 1) * 32 + lane));
-                g = hi > lo ? ((hi + 127u) >> 7) - (lo >> 7) : 0u;
-                G = g;
-#pragma unroll
-                for (int d = 16; d; d >>= 1) G += __shfl_xor_sync(0xFFFFFFFFu, G, d);
-                if (G <= kTeamXGroups) {
-                  xfast = true;
-                  break;
-                }
-                if (m == 1) break;
-                m = (m + 1) / 2;
-              }
-            } else {
-              m = K - k;
-            }
-            win_end = k + m;
-            if (xfast && G) {
-              uint32_t goff = g;  // exclusive prefix of the groups over the widths
-#pragma unroll
-              for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, goff, d);
-                if (lane >= d) goff += y;
-              }
-              goff -= g;
-              // value r of width w sits at xbuf[xrel[w] + r]
-              if (warp == 0) sts32(sb + LY::kXrel + 4u * (lane + 1), 128u * goff - (lo & ~127u));
-              for (uint32_t i = warp; i < G; i += kTeamWarps) {
-                const uint32_t own = __ballot_sync(0xFFFFFFFFu, g != 0 && goff <= i);
-                const int ow = 31 - __clz(own);
-                const uint32_t w = (uint32_t)ow + 1u;
-                const uint32_t gi = (__shfl_sync(0xFFFFFFFFu, lo, ow) >> 7) +
-                                    (i - __shfl_sync(0xFFFFFFFFu, goff, ow));
-                const uint32_t* src = page + __shfl_sync(0xFFFFFFFFu, dirv, ow) + (size_t)gi * 4u * w;
-                // lane = vertical slot: its four lanes' values are integers
-                // 4 lane .. 4 lane + 3 of the group
-                const uint32_t bit = (uint32_t)lane * w, sh = bit & 31u;
-                const uint32_t* rp = src + 4u * (bit >> 5);
-                uint4 a, b = make_uint4(0, 0, 0, 0);
-                const bool two = sh + w > 32u;
-                if (xal) {
-                  a = __ldg(reinterpret_cast<const uint4*>(rp));
-                  if (two) b = __ldg(reinterpret_cast<const uint4*>(rp + 4));
-                } else {
-                  a = make_uint4(__ldg(rp), __ldg(rp + 1), __ldg(rp + 2), __ldg(rp + 3));
-                  if (two) b = make_uint4(__ldg(rp + 4), __ldg(rp + 5), __ldg(rp + 6), __ldg(rp + 7));
-                }
-                const uint32_t mask = low_mask(w);
-                sts128(sb + LY::kXb + 512u * i + 16u * lane, funnel_r(a.x, b.x, sh) & mask,
-                       funnel_r(a.y, b.y, sh) & mask, funnel_r(a.z, b.z, sh) & mask,
-                       funnel_r(a.w, b.w, sh) & mask);
-              }
-            }
-            named_bar_sync(1, kTeamWarps * 32);  // the window's highs and xrel are in place
+          c_next = claim();
+          const izg_chunk ch = chunks[c];
+          int32_t st = precheck(IZG_SIMDFASTPFOR, kArray, ch.n);
+          const uint32_t* page = words + ch.word_off;
+          const uint32_t nb = (kArray ? ch.n / 128 * 128 : ch.n) / 128;
+          uint4 h = make_uint4(0, 0, 0, 0);
+          const uint4* rec = ix.page_rec(c);
+          bool decode = false;
+          if (st == IZG_OK && nb) {
+            h = ix.hdr[c];
+            st = (int32_t)(h.x & 0xFFu);
+            if (st == IZG_OK)
+              decode = true;
+            else if (!(st == IZG_E_FP_TRUNC_PAGE || st == IZG_E_FP_BA_OFFSET ||
+                       st == IZG_E_FP_TRUNC_BA) &&
+                     fp_positions_bad_idx(rec, reinterpret_cast<const uint8_t*>(page + h.w + 1),
+                                          (h.x >> 8) & 0xFFFFu, lane))
+              st = IZG_E_FP_POS_RANGE;
           }
-
-          // ---- this warp's four blocks ---------------------------------------
-          const uint32_t slot = git % kTeamSlots;
-          TEAM_PROF_T(pw1);
-          mbar_wait_s(sb + LY::kBar + 8u * slot, (git / kTeamSlots) & 1u);
-#ifdef IZG_TEAM_PROF
-          { const long long now = clock64(); pwin += pw1 - pw0; pfull += now - pw1; if (k == 0) pt2 = now; }
-#endif
-          const uint2 info = lds64(sb + LY::kInfo + 8u * slot);
-          const uint32_t blk0 = k * kTeamSI + 4u * warp;
-          const bool live = blk0 + q < nb;
-          // a block past the page's last decodes width 0 at the first block's rows
-          uint4 e = lds128(sb + LY::kRec + slot * (kTeamSI * 16u) + (live ? 16u * (4u * warp + q) : 0u));
-          if (!live) e.x = 0;
-          const uint32_t myb = e.x & 63u, myw = (e.x >> 6) & 63u, myc = e.x >> 12;
-          const uint32_t myoff = e.y, mybp = e.z, mycur = e.w;
-          const bool tot = __any_sync(0xFFFFFFFFu, myc != 0);
-          uint32_t v[4][4];
-          if (pal)
-            IZG_TEAM_UNPACK(info.x + 4u * myoff, myb, s8, v);
-          else
-            team_unpack_words(info.x + 4u * myoff, myb, s8, v);
-          if (tot) {
-            tile.wait_free();
-            tile.write(v);
-            __syncwarp();
-            if (xfast && info.y) {
-              const uint32_t xa = sb + LY::kXb + 4u * (lds32(sb + LY::kXrel + 4u * myw) + mycur);
-              bad |= team_patch(tile.t, info.y + mybp, xa, myb, myc, lane);
-            } else {
-              bad |= fp_patch<kVertical>(tile.t, page, ba, myb, myw, myc, mybp, mycur,
-                                         lds32(sb + LY::kDirb + 4u * myw), lane);
+          if (!decode) {
+            team_finish<DELTA>(st, 0, make_uint4(0, 0, 0, 0), ch, page, out + ch.out_off, c, status,
+                               consumed, lane);
+          } else {
+            const uint32_t A = h.w;
+            const bool ovf = (h.x >> 31) != 0;  // a cursor passed 65,535: no snapshots
+            const bool xal = (reinterpret_cast<uintptr_t>(page) & 15) == 0;
+            const uint32_t K = (nb + kTeamSI - 1) / kTeamSI;
+            const uint32_t ctx = sb + LY::kCtx + pp * LY::kCtxBytes;
+            // Super-iteration bounds, lane l <-> boundary l (0..16): packed
+            // word and byte-array offset of block 32 l, or the ends.
+            uint32_t bP = A, bS = 4u * (h.y - A - 1);
+            if ((uint32_t)lane * kTeamSI < nb) {
+              const uint4 e = rec[(uint32_t)lane * kTeamSI];
+              bP = e.y;
+              bS = e.z - 3u;
+            }
+            const uint32_t dirv = ix.dir[(size_t)c * 32 + lane];  // lane <-> width lane + 1
+            if (lane < 20) {
+              sts32(ctx + 4u * lane, bP);
+              sts32(ctx + 80u + 4u * lane, bS);
+            }
+            sts32(ctx + 160u + 4u * lane, dirv);
+            if (!ovf) {
+              const uint32_t* sp = reinterpret_cast<const uint32_t*>(ix.snap + (size_t)c * 512);
+#pragma unroll
+              for (int i = 0; i < 8; ++i)
+                sts32(ctx + kSnapOff + 4u * (lane + 32 * i), __ldg(sp + lane + 32 * i));
+            }
+            if (lane == 0) {
+              prefetch_l2(page + h.y, 4u * (h.z - h.y));  // exception arrays
+              sts128(ctx + kScal, c, nb, K, A);
+              sts128(ctx + kScal + 16, (ovf ? 1u : 0u) | (xal ? 2u : 0u), (uint32_t)ch.word_off,
+                     (uint32_t)(ch.word_off >> 32), 0);
+            }
+            if (pprep >= 2) mbar_wait_s(sb + LY::kPfree + 8u * pp, ((pprep >> 1) - 1u) & 1u);
+            sts32(sb + LY::kDirb + 4u * (36u * pp + lane + 1), dirv);
+            if (lane == 0) {
+              const uint32_t d = sb + LY::kDesc + 64u * pp;
+              sts128(d, c, ovf ? 2u : 0u, nb, K);
+              sts128(d + 16, A, h.z, ch.n, ch.n_words);
+              sts128(d + 32, (uint32_t)ch.word_off, (uint32_t)(ch.word_off >> 32),
+                     (uint32_t)ch.out_off, (uint32_t)(ch.out_off >> 32));
+              sts32(sb + LY::kDirb + 4u * 36u * pp, 0);
+              sts32(sb + LY::kBad + 4u * pp, 0);
             }
             __syncwarp();
-            tile.read(v);
+            if (lane == 0) mbar_arrive_s(sb + LY::kPfull + 8u * pp);
+            ++pprep;
+          }
+        }
+        progress = true;
+      }
+      // ---- stream (a): staging --------------------------------------------------
+      if (pa < pprep) {
+        const uint32_t ctx = sb + LY::kCtx + (pa & 1u) * LY::kCtxBytes;
+        uint32_t r = 0;  // bit 0: staged something, bit 1: page complete
+        if (lane == 0) {
+          const uint4 sc = lds128(ctx + kScal);        // c, nb, K, A
+          const uint4 sc2 = lds128(ctx + kScal + 16);  // flags, word_off
+          while (pr.gd < pr.gi &&
+                 mbar_test_s(sb + LY::kEmpty + 8u * (pr.gd % kTeamSlots), (pr.gd / kTeamSlots) & 1u))
+            ++pr.gd;
+          const uint32_t* page = words + ((uint64_t)sc2.z << 32 | sc2.y);
+          const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + sc.w + 1);
+          while (ka < sc.z && pr.gi < pr.gd + kTeamSlots) {
+            if (!team_issue(pr, sb, ctx, ka, sc.y, page, ba, ix.page_rec(sc.x))) break;
+            ++pr.gi;
+            ++ka;
+            r |= 1u;
+          }
+          if (ka == sc.z) r |= 2u;
+        }
+        r = __shfl_sync(0xFFFFFFFFu, r, 0);
+        ka = __shfl_sync(0xFFFFFFFFu, ka, 0);
+        if (r & 1u) progress = true;
+        if (r & 2u) {
+          ++pa;
+          ka = 0;
+          progress = true;
+        }
+      }
+      // ---- stream (b): exception windows ---------------------------------------
+      if (pb < pprep) {
+        const uint32_t ctx = sb + LY::kCtx + (pb & 1u) * LY::kCtxBytes;
+        const uint32_t xb = wprep & 1u;
+        const uint4 sc = lds128(ctx + kScal);        // c, nb, K, A
+        const uint4 sc2 = lds128(ctx + kScal + 16);  // flags, word_off
+        const uint32_t K = sc.z;
+        const bool ovf = (sc2.x & 1u) != 0;
+        uint32_t fr = 1;
+        if (wprep >= 2 && lane == 0)
+          fr = mbar_test_s(sb + LY::kXempty + 8u * xb, ((wprep >> 1) - 1u) & 1u);
+        if (__shfl_sync(0xFFFFFFFFu, fr, 0)) {
+          // lane <-> width w = lane + 1; lo / hi = its cursor at the window's
+          // ends; the longest window whose packed groups (16 w bytes each,
+          // plus the 16-byte alignment of each array's span) fit this half
+          const uint32_t w = (uint32_t)lane + 1u;
+          const uint32_t lo = (wkb && !ovf) ? lds16(ctx + kSnapOff + 2u * ((wkb - 1) * 32 + lane)) : 0u;
+          uint32_t m = K - wkb, g = 0, bytes = 0, tot = 0;
+          bool fast = false;
+          if (!ovf) {
+            for (;; --m) {
+              const uint32_t hi = lds16(ctx + kSnapOff + 2u * ((wkb + m - 1) * 32 + lane));
+              g = hi > lo ? ((hi + 127u) >> 7) - (lo >> 7) : 0u;
+              bytes = g ? g * 16u * w + 32u : 0u;
+              tot = bytes;
+#pragma unroll
+              for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(0xFFFFFFFFu, tot, d);
+              if (tot <= kTeamXb) {
+                fast = true;
+                break;
+              }
+              if (m == 1) break;
+            }
+          }
+          const uint32_t bar = sb + LY::kXfull + 8u * xb;
+          if (fast && tot) {
+            uint32_t off = bytes;  // exclusive prefix of the spans over the widths
+#pragma unroll
+            for (uint32_t d = 1; d < 32; d <<= 1) shfl_up_add(off, d);
+            off -= bytes;
+            const uint32_t* page = words + ((uint64_t)sc2.z << 32 | sc2.y);
+            const uint32_t* src = page + lds32(ctx + 160u + 4u * lane) + (size_t)(lo >> 7) * 4u * w;
+            const uintptr_t s0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
+            const uintptr_t s1 = (reinterpret_cast<uintptr_t>(src) + g * 16u * w + 15) & ~uintptr_t(15);
+            const uint32_t len = g ? (uint32_t)(s1 - s0) : 0u;  // <= bytes - 16
+            const uint32_t dst = sb + LY::kXb + xb * kTeamXb + off;
+            uint32_t sum = len;
+#pragma unroll
+            for (int d = 16; d; d >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, d);
+            // value r of width w: packed group r / 128 - lo / 128 from this address on
+            if (g)
+              sts64(sb + LY::kXrel + 8u * (36u * xb + w),
+                    dst + (uint32_t)(reinterpret_cast<uintptr_t>(src) - s0), lo & ~127u);
+            if (lane == 0) {
+              sts64(sb + LY::kXinfo + 8u * xb, wkb + m, 1u);
+              fence_proxy_async_smem();
+              mbar_arrive_expect_tx_s(bar, sum);
+            }
+            __syncwarp();
+            if (g) bulk_g2s_s(dst, reinterpret_cast<const void*>(s0), len, bar, pr.policy);
+          } else {
+            if (lane == 0) {
+              sts64(sb + LY::kXinfo + 8u * xb, wkb + m, fast ? 1u : 0u);
+              mbar_arrive_s(bar);
+            }
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive_s(sb + LY::kEmpty + 8u * slot);  // done with the staging
-          if (kArray) {
-            uint4 ex, incl;
-            uint32_t q3[4] = {0, 0, 0, 0};
-            team_scan_local<DELTA>(v, ex, incl, q3, lane);
-            // carry chain: the prefix up to the previous warp iteration arrives
-            // in this warp's mailbox; post ours to the next warp's
+          ++wprep;
+          wkb += m;
+          if (wkb >= K) {
+            ++pb;
+            wkb = 0;
+          }
+          progress = true;
+        }
+      }
+      if (ended && pa == pprep && pb == pprep) break;
+#ifdef IZG_TEAM_PROF
+      if (!progress && lane == 0) TEAM_PROF_ADD(6, 1);
+#endif
+      if (!progress) __nanosleep(64);
+    }
+    return;
+  }
+
+  // ========================= decoding warps ==================================
+  constexpr int NC = DELTA == IZG_DELTA_D4 ? 4 : DELTA == IZG_DELTA_D2 ? 2 : 1;
+  (void)NC;
+  const uint32_t q = lane >> 3, s8 = lane & 7;
+  TeamTile tile;
+  tile.init(sb + LY::kTiles + warp * kStageOut, lane, &omap);
+  uint32_t git = 0;     // super-iterations consumed so far, all pages (slot and parity)
+  uint32_t wcount = 0;  // exception windows entered so far
+  for (uint32_t pcount = 0;; ++pcount) {
+    const uint32_t pp = pcount & 1u;
+    TEAM_PROF_T(pq0);
+    mbar_wait_s(sb + LY::kPfull + 8u * pp, (pcount >> 1) & 1u);
+    TEAM_PROF_T(pq1);
+#ifdef IZG_TEAM_PROF
+    long long pxw = 0, pfw = 0, pmw = 0;
+#endif
+    const uint4 d0 = lds128(sb + LY::kDesc + 64u * pp);
+    if (d0.y & 1u) break;
+    const uint4 d1 = lds128(sb + LY::kDesc + 64u * pp + 16);
+    const uint4 d2 = lds128(sb + LY::kDesc + 64u * pp + 32);
+    const uint32_t c = d0.x, nb = d0.z, K = d0.w, A = d1.x;
+    izg_chunk ch;
+    ch.word_off = (uint64_t)d2.y << 32 | d2.x;
+    ch.out_off = (uint64_t)d2.w << 32 | d2.z;
+    ch.n = d1.z;
+    ch.n_words = d1.w;
+    const uint32_t* page = words + ch.word_off;
+    uint32_t* o = out + ch.out_off;
+    const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + A + 1);
+    const bool oal = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+    const int64_t orow = tma_out && (ch.out_off & 31) == 0 ? (int64_t)(ch.out_off >> 5) : -1;
+    const bool pal = (reinterpret_cast<uintptr_t>(page + 1) & 15) == 0;  // packed rows aligned
+    uint32_t win_end = 0, xb = 0;
+    bool xfast = false, bad = false;
+    uint4 fin = make_uint4(0, 0, 0, 0);  // warp 7, lane 31: the page's final carry
+#pragma unroll 1
+    for (uint32_t k = 0; k < K; ++k, ++git) {
+      if (k == win_end) {  // next exception window
+        if (k) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive_s(sb + LY::kXempty + 8u * xb);
+        }
+        xb = wcount & 1u;
+        TEAM_PROF_T(px0);
+        mbar_wait_s(sb + LY::kXfull + 8u * xb, (wcount >> 1) & 1u);
+#ifdef IZG_TEAM_PROF
+        pxw += clock64() - px0;
+#endif
+        const uint2 xi = lds64(sb + LY::kXinfo + 8u * xb);
+        win_end = xi.x;
+        xfast = xi.y != 0;
+        ++wcount;
+      }
+      const uint32_t slot = git % kTeamSlots;
+      TEAM_PROF_T(pf0);
+      mbar_wait_s(sb + LY::kBar + 8u * slot, (git / kTeamSlots) & 1u);
+#ifdef IZG_TEAM_PROF
+      pfw += clock64() - pf0;
+#endif
+      const uint2 info = lds64(sb + LY::kInfo + 8u * slot);
+      const uint32_t blk0 = k * kTeamSI + 4u * warp;
+      const bool live = blk0 + q < nb;
+      // a block past the page's last decodes width 0 at the first block's rows
+      uint4 e = lds128(sb + LY::kRec + slot * (kTeamSI * 16u) + (live ? 16u * (4u * warp + q) : 0u));
+      if (!live) e.x = 0;
+      const uint32_t myb = e.x & 63u, myw = (e.x >> 6) & 63u, myc = e.x >> 12;
+      const uint32_t myoff = e.y, mybp = e.z, mycur = e.w;
+      const bool tot = __any_sync(0xFFFFFFFFu, myc != 0);
+      uint32_t v[4][4];
+      if (pal)
+        IZG_TEAM_UNPACK(info.x + 4u * myoff, myb, s8, v);
+      else
+        team_unpack_words(info.x + 4u * myoff, myb, s8, v);
+      if (tot) {
+        tile.wait_free();
+        tile.write(v);
+        __syncwarp();
+        if (xfast && info.y) {
+          const uint2 xr = lds64(sb + LY::kXrel + 8u * (36u * xb + myw));
+          bad |= team_patch(tile.t, info.y + mybp, xr.x, mycur - xr.y, myw, myb, myc, lane);
+        } else {
+          bad |= fp_patch<kVertical>(tile.t, page, ba, myb, myw, myc, mybp, mycur,
+                                     lds32(sb + LY::kDirb + 4u * (36u * pp + myw)), lane);
+        }
+        __syncwarp();
+        tile.read(v);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_s(sb + LY::kEmpty + 8u * slot);  // done with the staging
+      if (kArray) {
+        uint4 ex, incl;
+        uint32_t q3[4] = {0, 0, 0, 0};
+        team_scan_local<DELTA>(v, ex, incl, q3, lane);
+        // carry chain: the prefix up to the previous warp iteration arrives
+        // in this warp's mailbox; ours goes to the next warp's (the page's
+        // last one posts the next page's zero carry instead)
 #ifndef IZG_ABL_TEAM_NOCHAIN  // developer ablation (wrong output): no wait on the carry chain
-            TEAM_PROF_T(pm0);
-            mbar_wait_s(sb + LY::kMbx + 8u * warp, git & 1u);
+        TEAM_PROF_T(pm0);
+        mbar_wait_s(sb + LY::kMbx + 8u * warp, git & 1u);
 #ifdef IZG_TEAM_PROF
-            pmbx += clock64() - pm0;
+        pmw += clock64() - pm0;
 #endif
 #endif
-            const uint4 pv = lds128(sb + LY::kTot + 16u * warp);
-            __syncwarp();  // everyone has read the mailbox before the chain can refill it
-            if (lane == 31) {
-              const bool last = warp == kTeamWarps - 1;
-              const uint32_t dst = last ? (k + 1 == K ? kTeamWarps : 0) : warp + 1;
-              sts128(sb + LY::kTot + 16u * dst, pv.x + incl.x, pv.y + incl.y, pv.z + incl.z,
-                     pv.w + incl.w);
-              if (dst != kTeamWarps) mbar_arrive_s(sb + LY::kMbx + 8u * dst);
-            }
-            team_scan_apply<DELTA>(v, u4add(pv, ex), q3);
-          }
-          if (orow >= 0 && blk0 + 4 <= nb) {
-            if (!tot) tile.wait_free();
-            tile.write(v);
-            tile.store((uint32_t)(orow + 4 * (int64_t)blk0));
-          } else {
-            __syncwarp();
-            if (live) store_direct(v, o + (size_t)(blk0 + q) * 128 + 16 * s8, oal);
-          }
+        const uint4 pv = lds128(sb + LY::kTot + 16u * warp);
+        __syncwarp();  // everyone has read the mailbox before the chain can refill it
+        if (lane == 31) {
+          fin = u4add(pv, incl);
+          const bool wrap = warp == kTeamWarps - 1;
+          const uint32_t dst = wrap ? 0u : (uint32_t)warp + 1u;
+          if (wrap && k + 1 == K)
+            sts128(sb + LY::kTot, 0, 0, 0, 0);
+          else
+            sts128(sb + LY::kTot + 16u * dst, fin.x, fin.y, fin.z, fin.w);
+          mbar_arrive_s(sb + LY::kMbx + 8u * dst);
         }
-        if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) s_page[1] = 1;
-#ifdef IZG_TEAM_PROF
-        if (tid == 0) {
-          const long long pt3 = clock64();
-          TEAM_PROF_ADD(0, 1); TEAM_PROF_ADD(1, pt1 - pt0); TEAM_PROF_ADD(2, pt2 - pt1);
-          TEAM_PROF_ADD(3, pwin); TEAM_PROF_ADD(4, pt3 - pt2); TEAM_PROF_ADD(6, pfull);
-          TEAM_PROF_ADD(7, pmbx);
-          s_page[2] = (uint32_t)pt3;
-        }
-#endif
-        }  // decoding warps
-        pos = h.z;
+        team_scan_apply<DELTA>(v, u4add(pv, ex), q3);
+      }
+      if (orow >= 0 && blk0 + 4 <= nb) {
+        if (!tot) tile.wait_free();
+        tile.write(v);
+        tile.store((uint32_t)(orow + 4 * (int64_t)blk0));
+      } else {
+        __syncwarp();
+        if (live) store_direct(v, o + (size_t)(blk0 + q) * 128 + 16 * s8, oal);
       }
     }
-    __syncthreads();  // bad flag, final carry; s_page[0] read by everyone before the next claim
+    // ---- end of the page ------------------------------------------------------
 #ifdef IZG_TEAM_PROF
-    if (tid == 0 && decoded) TEAM_PROF_ADD(5, (uint32_t)((uint32_t)clock64() - s_page[2]));
+    if (tid == 0) {
+      TEAM_PROF_ADD(0, 1); TEAM_PROF_ADD(1, pq1 - pq0); TEAM_PROF_ADD(2, pxw); TEAM_PROF_ADD(3, pfw);
+      TEAM_PROF_ADD(4, pmw); TEAM_PROF_ADD(5, clock64() - pq0);
+    }
 #endif
-    if (warp == 0) {
-      if (decoded && s_page[1]) st = IZG_E_FP_POS_RANGE;
-      if (decoded && kArray) carry = lds128(sb + LY::kTot + 16u * kTeamWarps);
+    __syncwarp();
+    if (lane == 0) mbar_arrive_s(sb + LY::kXempty + 8u * xb);  // done with its last window
+    if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) sts32(sb + LY::kBad + 4u * pp, 1);
+    if (warp != kTeamWarps - 1) {
       __syncwarp();
-      if (kArray && st == IZG_OK) {
-        if (core < ch.n) {  // Variable Byte remainder (codec.cpp:56-62)
-          uint32_t rb = 0;
-          if (lane == 0)
-            st = vbyte_tail<DELTA>(reinterpret_cast<const uint8_t*>(page + pos),
-                                   4u * (ch.n_words - pos), core, ch.n - core, carry, o, &rb);
-          st = __shfl_sync(0xFFFFFFFFu, st, 0);
-          rb = __shfl_sync(0xFFFFFFFFu, rb, 0);
-          if (st == IZG_OK) pos += (rb + 3) / 4;
-        }
-        if (st == IZG_OK && pos != ch.n_words) st = IZG_E_PAYLOAD_SIZE;  // codec.cpp:63-64
-      }
-      if (lane == 0) {
-        status[c] = st;
-        if (consumed) consumed[c] = st == IZG_OK ? pos : 0;
-      }
+      if (lane == 0) mbar_arrive_s(sb + LY::kPdone + 8u * pp);
+    } else {  // the last warp of the chain holds the final carry: it ends the chunk
+      mbar_wait_s(sb + LY::kPdone + 8u * pp, (pcount >> 1) & 1u);
+      uint4 carry;
+      carry.x = __shfl_sync(0xFFFFFFFFu, fin.x, 31);
+      carry.y = __shfl_sync(0xFFFFFFFFu, fin.y, 31);
+      carry.z = __shfl_sync(0xFFFFFFFFu, fin.z, 31);
+      carry.w = __shfl_sync(0xFFFFFFFFu, fin.w, 31);
+      const int32_t st = lds32(sb + LY::kBad + 4u * pp) ? IZG_E_FP_POS_RANGE : IZG_OK;
+      team_finish<DELTA>(st, d1.y, carry, ch, page, o, c, status, consumed, lane);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_s(sb + LY::kPfree + 8u * pp);
     }
   }
-  if (warp < kTeamWarps) tile.drain();
+  tile.drain();
 }
 
 }  // namespace izg

@@ -21,7 +21,8 @@ L.izg_debug_team_prof(buf.ctypes.data, 1)
 b.decode(); torch.cuda.synchronize()
 L.izg_debug_team_prof(buf.ctypes.data, 0)
 n = float(buf[0])
-names = ["claim->setup barrier", "setup->first staging landed", "window set-ups", "iterations (first landed->loop end)",
-         "loop end->page end", "warp0 waits on full", "warp0 waits on mailbox"]
+names = ["warp 0 waits: page descriptor", "warp 0 waits: exception window", "warp 0 waits: staged data",
+         "warp 0 waits: carry mailbox", "warp 0: whole page", "staging warp: idle passes",
+         "staging warp: cycles in unpack passes"]
 for nm, v in zip(names, buf[1:]):
-    print(f"{nm:40s} {float(v) / n:10.0f} cycles/page")
+    print(f"{nm:40s} {float(v) / n:10.0f} per page")
