@@ -105,17 +105,26 @@ size_t team_smem_bytes();
 int team_threads();
 
 // Indexed SIMD-FastPFOR batches of at least IZG_TEAM_MIN pages decode with
-// the team kernel (team.cuh).  IZG_TEAM=0 / 1 forces it off / on.
+// the team kernel (team.cuh: one CTA of 8 decoding warps + a staging warp
+// per page).  Measured on B200 (tools/team_sweep.py, 65,536-integer pages,
+// ms, team vs the path taken otherwise; C5 data / C4 10 % outliers): 64
+// pages 0.093 vs 0.092 (split) / 0.142 vs 0.137; 256: 0.103 vs 0.129 / 0.152
+// vs 0.186; 1,024: 0.192 vs 0.259 / 0.249 vs 0.357; 2,048: 0.269 vs 0.353
+// (one warp per page) / 0.379 vs 0.564; 8,192: 0.867 vs 0.997 / 1.30 vs
+// 1.72; 32,768: 3.08 vs 3.15 / 4.17 vs 5.08.  IZG_TEAM=0 / 1 forces it off /
+// on; IZG_SPLIT=1 (the split kernel forced) also turns it off.
 #ifndef IZG_TEAM_MIN
-#define IZG_TEAM_MIN 0xFFFFFFFFu
+#define IZG_TEAM_MIN 128
 #endif
+int env_switch(const char* name) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : -1;
+}
 bool team_wanted(uint32_t n_chunks) {
-  static const int force = [] {
-    const char* e = std::getenv("IZG_TEAM");
-    return e ? std::atoi(e) : -1;
-  }();
+  static const int force = env_switch("IZG_TEAM");
+  static const int split_force = env_switch("IZG_SPLIT");
   if (force >= 0) return force != 0;
-  return n_chunks >= IZG_TEAM_MIN;
+  return split_force != 1 && n_chunks >= IZG_TEAM_MIN;
 }
 
 // SIMD-BP128 array-mode batches of up to IZG_CTA_MAX chunks take the
@@ -350,7 +359,8 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                       : idx   ? Layout<IZG_SIMDFASTPFOR, true>::kSmem
                       : paged ? Layout<IZG_SIMDFASTPFOR>::kSmem
                               : Layout<IZG_SIMDBP128>::kSmem;
-  const bool split = !probe && split_wanted(codec, n_chunks) && d_ws &&
+  const bool team = idx && team_wanted(n_chunks);
+  const bool split = !team && !probe && split_wanted(codec, n_chunks) && d_ws &&
                      (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
                      ws_bytes >= workspace_bytes(codec, n_chunks);
   const void* kfn = split ? reinterpret_cast<const void*>(pick_split(codec, delta))
@@ -441,7 +451,7 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     ix = idx_view(d_ws, n_chunks);
   }
   if (cudaMemsetAsync(counter, 0, sizeof(uint32_t), s) != cudaSuccess) return IZG_ERR_CUDA;
-  if (idx && !split && team_wanted(n_chunks)) {
+  if (team) {
     TeamFn tfn = pick_team(delta);
     int tper_sm = 0, tsms = 0;
     uint32_t* tcounter = nullptr;

@@ -42,7 +42,10 @@ namespace izg {
 
 constexpr int kTeamWarps = 8;
 constexpr uint32_t kTeamSI = 4 * kTeamWarps;  // blocks per super-iteration
-constexpr uint32_t kTeamSlots = 4;            // super-iterations staged ahead
+#ifndef IZG_TEAM_SLOTS
+#define IZG_TEAM_SLOTS 4
+#endif
+constexpr uint32_t kTeamSlots = IZG_TEAM_SLOTS;  // super-iterations staged ahead
 #ifndef IZG_TEAM_PK
 #define IZG_TEAM_PK 16896
 #endif
@@ -370,6 +373,22 @@ struct TeamProducer {
   uint32_t pk_head, ps_head;  // allocation heads of the two staging buffers
   uint64_t policy;
 };
+
+// Wait with a suspend-time hint: the waiting warp sleeps in hardware until
+// the phase completes (or the hint expires) instead of re-issuing try_wait.
+#ifndef IZG_TEAM_WAIT_NS
+#define IZG_TEAM_WAIT_NS 4000
+#endif
+__device__ __forceinline__ void team_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "TW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra TW_%=;\n\t}"
+      :
+      : "r"(bar), "r"(parity), "r"((uint32_t)IZG_TEAM_WAIT_NS)
+      : "memory");
+}
 
 __device__ __forceinline__ bool mbar_test_s(uint32_t bar, uint32_t parity) {
   uint32_t ok;
@@ -758,7 +777,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
   for (uint32_t pcount = 0;; ++pcount) {
     const uint32_t pp = pcount & 1u;
     TEAM_PROF_T(pq0);
-    mbar_wait_s(sb + LY::kPfull + 8u * pp, (pcount >> 1) & 1u);
+    team_wait(sb + LY::kPfull + 8u * pp, (pcount >> 1) & 1u);
     TEAM_PROF_T(pq1);
 #ifdef IZG_TEAM_PROF
     long long pxw = 0, pfw = 0, pmw = 0;
@@ -791,7 +810,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
         }
         xb = wcount & 1u;
         TEAM_PROF_T(px0);
-        mbar_wait_s(sb + LY::kXfull + 8u * xb, (wcount >> 1) & 1u);
+        team_wait(sb + LY::kXfull + 8u * xb, (wcount >> 1) & 1u);
 #ifdef IZG_TEAM_PROF
         pxw += clock64() - px0;
 #endif
@@ -802,7 +821,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
       }
       const uint32_t slot = git % kTeamSlots;
       TEAM_PROF_T(pf0);
-      mbar_wait_s(sb + LY::kBar + 8u * slot, (git / kTeamSlots) & 1u);
+      team_wait(sb + LY::kBar + 8u * slot, (git / kTeamSlots) & 1u);
 #ifdef IZG_TEAM_PROF
       pfw += clock64() - pf0;
 #endif
@@ -845,7 +864,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
         // last one posts the next page's zero carry instead)
 #ifndef IZG_ABL_TEAM_NOCHAIN  // developer ablation (wrong output): no wait on the carry chain
         TEAM_PROF_T(pm0);
-        mbar_wait_s(sb + LY::kMbx + 8u * warp, git & 1u);
+        team_wait(sb + LY::kMbx + 8u * warp, git & 1u);
 #ifdef IZG_TEAM_PROF
         pmw += clock64() - pm0;
 #endif
@@ -887,7 +906,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
       __syncwarp();
       if (lane == 0) mbar_arrive_s(sb + LY::kPdone + 8u * pp);
     } else {  // the last warp of the chain holds the final carry: it ends the chunk
-      mbar_wait_s(sb + LY::kPdone + 8u * pp, (pcount >> 1) & 1u);
+      team_wait(sb + LY::kPdone + 8u * pp, (pcount >> 1) & 1u);
       uint4 carry;
       carry.x = __shfl_sync(0xFFFFFFFFu, fin.x, 31);
       carry.y = __shfl_sync(0xFFFFFFFFu, fin.y, 31);

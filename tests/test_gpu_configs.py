@@ -6,12 +6,13 @@ decode_array / decode_deltas word for word: the fused kernels (izg_decode),
 the workspace path (izg_decode_ws: page index + indexed decode, or the split
 kernel for small batches), the host-buffer path (izg_decode_host), and —
 in fresh processes, since the switches are read once — the one-warp
-indexed path (IZG_SPLIT=0), the split kernel everywhere (IZG_SPLIT=1), the
+indexed path (IZG_SPLIT=0 IZG_TEAM=0), the split kernel everywhere (IZG_SPLIT=1), the
 large-batch indexed shape (IZG_BIG_IDX_BATCH=1) and the SIMD-BP128 group
 kernels (IZG_GROUP=2/8) and the lane-per-page index pass
 (IZG_INDEX_LANES_MIN=0), each with the CTA kernel off (IZG_CTA=0; it is the
 default for these small SIMD-BP128 batches and is forced onto the same
-cases by tests/test_gpu_cta.py)."""
+cases by tests/test_gpu_cta.py).  The team SIMD-FastPFOR kernel (the default
+from 128 pages on) is forced onto the same cases by tests/test_gpu_team.py."""
 import os
 import subprocess
 import sys
@@ -35,12 +36,13 @@ def test_default_paths(cuda, cases):
     CC.check_gpu(cases)
 
 
-@pytest.mark.parametrize("env", [{"IZG_SPLIT": "0", "IZG_CTA": "0"},
+@pytest.mark.parametrize("env", [{"IZG_SPLIT": "0", "IZG_CTA": "0", "IZG_TEAM": "0"},
                                  {"IZG_SPLIT": "1", "IZG_CTA": "0"},
-                                 {"IZG_SPLIT": "0", "IZG_BIG_IDX_BATCH": "1", "IZG_CTA": "0"},
+                                 {"IZG_SPLIT": "0", "IZG_BIG_IDX_BATCH": "1", "IZG_CTA": "0",
+                                  "IZG_TEAM": "0"},
                                  {"IZG_SPLIT": "0", "IZG_GROUP": "2", "IZG_CTA": "0"},
                                  {"IZG_SPLIT": "0", "IZG_GROUP": "8", "IZG_CTA": "0"},
-                                 {"IZG_SPLIT": "0", "IZG_INDEX_LANES_MIN": "0"}],
+                                 {"IZG_SPLIT": "0", "IZG_INDEX_LANES_MIN": "0", "IZG_TEAM": "0"}],
                          ids=["one-warp", "split", "big-idx", "group2", "group8", "lane-index"])
 def test_forced_paths(cuda, ref, env):
     r = subprocess.run([sys.executable, "-m", "tests.config_cases"], cwd=ROOT,

@@ -243,13 +243,13 @@ def test_large_batch_shape():
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, IZG_BIG_IDX_BATCH="1", IZG_SPLIT="0")
+    env = dict(os.environ, IZG_BIG_IDX_BATCH="1", IZG_SPLIT="0", IZG_TEAM="0")
     r = subprocess.run([sys.executable, "-c", _BIG.format(root=root)], env=env,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("env", [{"IZG_INDEX_LANES_MIN": "0", "IZG_SPLIT": "0"},
+@pytest.mark.parametrize("env", [{"IZG_INDEX_LANES_MIN": "0", "IZG_SPLIT": "0", "IZG_TEAM": "0"},
                                  {"IZG_INDEX_LANES_MIN": "0", "IZG_SPLIT": "1"}],
                          ids=["indexed", "split"])
 def test_lane_index_pass(env):
