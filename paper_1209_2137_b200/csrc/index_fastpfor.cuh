@@ -370,7 +370,9 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
         lst = IZG_E_FP_EXHAUSTED;
     }
     if (lst == IZG_OK && packed + 4 * b > A) lst = IZG_E_FP_OVERRUN;
+#ifndef IZG_ABL_IDX_NOREC  // developer ablation (decode broken): no record stores
     stg128_cg(rec + k, make_uint4(e, packed, s + 3, cur));
+#endif
     packed += 4 * b;
     s += cc ? 3 + cc : 2;
     if ((k & 31u) == 31u || k + 1 == nblocks) {  // cursors after 32 (k / 32 + 1) blocks

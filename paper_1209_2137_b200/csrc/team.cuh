@@ -58,6 +58,9 @@ constexpr uint32_t kTeamXb = IZG_TEAM_XB;     // packed exception arrays of a wi
 #ifndef IZG_TEAM_UNPACK
 #define IZG_TEAM_UNPACK team_unpack_window  // or team_unpack_rows (more row loads, fewer moves)
 #endif
+#ifndef IZG_TEAM_NARROW
+#define IZG_TEAM_NARROW 1  // separate unpack for iterations whose four widths are all <= 8
+#endif
 #ifndef IZG_TEAM_AHEAD
 #define IZG_TEAM_AHEAD 2  // warp 0 stages more once fewer than this many lie ahead
 #endif
@@ -224,6 +227,28 @@ __device__ __forceinline__ void team_unpack_rows(uint32_t bb, uint32_t width, ui
   }
 }
 
+// Widths up to 8: the lane's four slots are 4 b <= 32 consecutive bits of each
+// vertical lane's stream, inside two rows: one funnel shift per lane brings
+// them into a word, then a shift and a mask per value.
+__device__ __forceinline__ void team_unpack_narrow(uint32_t bb, uint32_t width, uint32_t s8,
+                                                   uint32_t (&v)[4][4]) {
+  const uint32_t mask = (1u << width) - 1u;
+  const uint32_t bit = 4u * s8 * width;
+  const uint32_t ra = bb + 16u * (bit >> 5), sh = bit & 31u;
+  const uint4 lo = lds128(ra);
+  const uint4 hi = lds128(ra + 16u);
+  const uint32_t w0 = funnel_r(lo.x, hi.x, sh), w1 = funnel_r(lo.y, hi.y, sh);
+  const uint32_t w2 = funnel_r(lo.z, hi.z, sh), w3 = funnel_r(lo.w, hi.w, sh);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint32_t s = c * width;
+    v[c][0] = (w0 >> s) & mask;
+    v[c][1] = (w1 >> s) & mask;
+    v[c][2] = (w2 >> s) & mask;
+    v[c][3] = (w3 >> s) & mask;
+  }
+}
+
 __device__ __forceinline__ void team_unpack_window(uint32_t bb, uint32_t width, uint32_t s8,
                                                    uint32_t (&v)[4][4]) {
   unpack_slots_aligned(LinBuf{0u}, bb, width, s8, v);
@@ -379,8 +404,24 @@ struct TeamProducer {
 #ifndef IZG_TEAM_WAIT_NS
 #define IZG_TEAM_WAIT_NS 4000
 #endif
+#ifndef IZG_TEAM_WAIT_SLEEP
+#define IZG_TEAM_WAIT_SLEEP 0  // ns slept between polls (0: re-issue try_wait at once)
+#endif
 __device__ __forceinline__ void team_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
+#if IZG_TEAM_WAIT_SLEEP
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@p bra TD_%=;\n\t"
+      "TW_%=:\n\t"
+      "nanosleep.u32 %3;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra TW_%=;\n\t"
+      "TD_%=:\n\t}"
+      :
+      : "r"(bar), "r"(parity), "r"((uint32_t)IZG_TEAM_WAIT_NS), "r"((uint32_t)IZG_TEAM_WAIT_SLEEP)
+      : "memory");
+#else
       "{\n\t.reg .pred p;\n\t"
       "TW_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
@@ -388,6 +429,7 @@ __device__ __forceinline__ void team_wait(uint32_t bar, uint32_t parity) {
       :
       : "r"(bar), "r"(parity), "r"((uint32_t)IZG_TEAM_WAIT_NS)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ bool mbar_test_s(uint32_t bar, uint32_t parity) {
@@ -835,10 +877,16 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
       const uint32_t myoff = e.y, mybp = e.z, mycur = e.w;
       const bool tot = __any_sync(0xFFFFFFFFu, myc != 0);
       uint32_t v[4][4];
-      if (pal)
-        IZG_TEAM_UNPACK(info.x + 4u * myoff, myb, s8, v);
-      else
+      if (pal) {
+#if IZG_TEAM_NARROW
+        if (__all_sync(0xFFFFFFFFu, myb <= 8u))
+          team_unpack_narrow(info.x + 4u * myoff, myb, s8, v);
+        else
+#endif
+          IZG_TEAM_UNPACK(info.x + 4u * myoff, myb, s8, v);
+      } else {
         team_unpack_words(info.x + 4u * myoff, myb, s8, v);
+      }
       if (tot) {
         tile.wait_free();
         tile.write(v);

@@ -10,6 +10,6 @@ tail -1 $OUT/bench.log
 $NCU --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
 echo launches rc=$?
-$NCU --set full --import-source on --clock-control none -k regex:"decode_kernel|fp_index" -s 3 -c 3 \
+$NCU --set full --import-source on --clock-control none -k regex:"decode_kernel|fp_index|fp_team" -s 3 -c 3 \
     -o $OUT/c5_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_full.log 2>&1
 echo full rc=$?
