@@ -743,7 +743,8 @@ def main():
                 "verified": mism == 0, "prep_s_rank0": round(prep_s, 1),
             },
             "roofline": {"bound": "hbm",
-                         "kernel": (f"fp_index_kernel+decode_kernel[{dom}] (events around both)"
+                         "kernel": (f"fp_index_lanes_kernel+fp_team_kernel[{dom}] (page index pass + "
+                                    "team decode, events around both)"
                                     if batches[dom].launches_per_decode == 2
                                     else f"decode_kernel[{dom}]"),
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -1,35 +1,42 @@
-// team.cuh — SIMD-FastPFOR decode with one CTA (a "team" of 8 warps) per page.
+// team.cuh — SIMD-FastPFOR decode with one CTA (a "team": 8 decoding warps
+// and a staging warp) per page, from the records of the page index pass
+// (index_fastpfor.cuh).  DESIGN.md 3 has the measurements and the history.
 //
-// The warp-per-page decode (decode_fastpfor.cuh / index_fastpfor.cuh) is
-// issue-bound: every warp runs its own staging ring, and every exception
-// costs two scattered global loads plus the address arithmetic of the
-// vertical layout (codec_patched.cpp:338-379 bulk-unpacks the exception
-// arrays instead).  Here a CTA decodes one page in lockstep super-iterations
-// of 32 blocks (4,096 integers), one warp iteration of 4 blocks per warp:
+// The warp-per-page decode (decode_fastpfor.cuh / index_fastpfor.cuh) runs a
+// staging ring per warp and fetches every exception with two scattered global
+// loads plus the address arithmetic of the vertical layout, and a batch of a
+// few thousand pages leaves most of its warp slots empty.  Here a page is
+// decoded in super-iterations of 32 blocks (4,096 integers), one warp
+// iteration of 4 blocks per decoding warp:
 //
-//   * staging is shared: per super-iteration one thread issues TMA bulk
-//     copies of the packed words, the 32 block records of the page index
-//     pass and the position bytes into linear shared-memory buffers (one
-//     mbarrier per slot, four slots in flight), so no warp manages a ring;
-//   * exception highs are bulk-unpacked the way the reference does
-//     (codec_patched.cpp:346-379), but only for a WINDOW of super-iterations
-//     at a time: the page index pass records every width's cursor at each
-//     32-block boundary (IdxView::snap), the team takes the longest window
-//     whose vertical groups fit its 16 KiB buffer, and its warps unpack
-//     those groups (one warp per group of 128, lane = slot, straight from
-//     global memory).  A patch then costs one position byte and one value
-//     from shared memory (codec_patched.cpp:390-404: o[pos] |= high << b);
-//   * the prefix sum is two-level: each warp scans its 512 integers from a
-//     zero carry, lane 31 publishes the warp total, one CTA barrier, and
-//     every warp adds the page carry plus the totals of the warps before it
-//     (delta.cpp:60-75 for D4; the same split for D1 / D2 / DM).
+//   * the staging warp is the front end, ahead of the decoders.  It claims
+//     pages, settles the ones that need no decode, publishes a descriptor
+//     per page, and feeds two in-order streams of TMA bulk copies: (a) per
+//     super-iteration the packed words, the 32 block records and the
+//     position bytes, into linear staging buffers (one mbarrier per slot,
+//     four slots); (b) per exception WINDOW the packed exception arrays
+//     (codec_patched.cpp:346-379), one copy per width: the page index pass
+//     records every width's cursor at each 32-block boundary
+//     (IdxView::snap), and a window is the longest run of super-iterations
+//     whose groups fit half of the buffer;
+//   * a decoding warp waits for its slot, unpacks its four blocks from the
+//     staging buffer, and patches in its output tile with the position byte
+//     and the exception high both read from shared memory
+//     (codec_patched.cpp:390-404: o[pos] |= high << b);
+//   * the prefix sum is a carry chain: each warp scans its 512 integers from
+//     a zero carry, takes the running prefix from its mailbox, posts prefix +
+//     own total to the next warp's, adds the prefix and stores the tile with
+//     TMA (delta.cpp:60-75 for D4; the same split for D1 / D2 / DM).
 //
-// Everything the index pass checked stays checked there; exception
-// positions >= 128 are detected while patching (codec_patched.cpp:328-330),
-// as in the warp-per-page kernels.  Pages whose exception windows or
-// position bytes do not fit (a single super-iteration over 32 groups or
-// 5 KiB of positions, cursors past 65,535) patch from global memory with
-// fp_patch for the super-iterations concerned: same results.
+// No CTA barrier after initialisation: pages, windows, slots and mailboxes
+// are all handed over through mbarriers.  Everything the index pass checked
+// stays checked there; exception positions >= 128 are detected while
+// patching (codec_patched.cpp:328-330), as in the warp-per-page kernels.
+// What does not fit the staged paths (a super-iteration with over 5 KiB of
+// position bytes, a window that does not fit even for one super-iteration,
+// cursors past 65,535, packed rows that are not 16-byte aligned) is patched
+// from global memory with fp_patch / unpacked with word loads inside the
+// same kernel: same results (tests/test_gpu_team.py).
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -60,6 +67,9 @@ constexpr uint32_t kTeamXb = IZG_TEAM_XB;     // packed exception arrays of a wi
 #endif
 #ifndef IZG_TEAM_NARROW
 #define IZG_TEAM_NARROW 1  // separate unpack for iterations whose four widths are all <= 8
+#endif
+#ifndef IZG_TEAM_IDLE_NS
+#define IZG_TEAM_IDLE_NS 64  // staging warp: sleep after a pass without progress
 #endif
 #ifndef IZG_TEAM_AHEAD
 #define IZG_TEAM_AHEAD 2  // warp 0 stages more once fewer than this many lie ahead
@@ -803,7 +813,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
 #ifdef IZG_TEAM_PROF
       if (!progress && lane == 0) TEAM_PROF_ADD(6, 1);
 #endif
-      if (!progress) __nanosleep(64);
+      if (!progress) __nanosleep(IZG_TEAM_IDLE_NS);
     }
     return;
   }
