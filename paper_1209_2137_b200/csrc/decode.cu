@@ -189,12 +189,13 @@ constexpr uint32_t kSplitMaxChunksBp = 384, kSplitMaxChunksFp = 1024;
 constexpr uint32_t kBigIdxBatch = IZG_BIG_IDX_BATCH;
 // SIMD-FastPFOR page index pass: one lane per page from IZG_INDEX_LANES_MIN
 // pages on, one warp per page below (identical workspace contents).  The
-// lane walk is latency-bound (~0.35 ms whatever the batch up to ~8,192
-// pages), the warp walk issue-bound: measured (tools/index_probe.py, C5
-// pages, ms, lane / warp): 2,048: 0.35 / 0.08; 8,192: 0.36 / 0.19; 32,768:
-// 0.44 / 0.62; 65,536: 0.90 / 1.19.  IZG_INDEX_LANES_MIN=0 / huge forces it.
+// lane walk is latency-bound (~0.4 ms whatever the batch: every page's walk
+// runs at once), the warp walk issue-bound: measured (tools/idx_only.py, C5
+// pages, ms, lane / warp): 8,192: 0.39 / 0.19; 16,384: 0.40 / 0.34; 32,768:
+// 0.46 / 0.62; 65,536: 0.49 / 1.19 (round 2's first lane walk, loading each
+// entry from global memory: 0.93).  IZG_INDEX_LANES_MIN=0 / huge forces it.
 #ifndef IZG_INDEX_LANES_MIN
-#define IZG_INDEX_LANES_MIN 16384
+#define IZG_INDEX_LANES_MIN 20480
 #endif
 bool split_wanted(int codec, uint32_t n_chunks) {
   if (codec != IZG_SIMDBP128 && codec != IZG_SIMDFASTPFOR) return false;
@@ -427,6 +428,11 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                            cudaFuncAttributeMaxDynamicSharedMemorySize, b);
       cudaFuncSetAttribute(fp_index_kernel<true, kVertical>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+      const int bl = (int)IdxLaneLayout::kSmem;
+      cudaFuncSetAttribute(fp_index_lanes_kernel<false, kVertical>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, bl);
+      cudaFuncSetAttribute(fp_index_lanes_kernel<true, kVertical>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, bl);
       return true;
     }();
     (void)attr;

@@ -29,6 +29,8 @@
 //                 for the team decode's exception windows (team.cuh); bit 31
 //                 of hdr.x is set when a cursor passed 65,535 (rows invalid)
 #pragma once
+#include <cstdio>
+
 #include "decode_fastpfor.cuh"
 #include "izg_common.cuh"
 
@@ -224,11 +226,33 @@ constexpr int kIdxLaneWarps = 4;
 #define IZG_IDXL_AHEAD 256  // 65,536 C5 pages: 128 / 256 / 512 / 1024 B ahead -> 0.93 / 0.90 / 1.00 / 1.10 ms
 #endif
 constexpr uint32_t kIdxLaneAhead = IZG_IDXL_AHEAD;  // bytes the L1 prefetches run ahead of the walk
+// The walk reads the byte array from a per-lane ring in shared memory that
+// the lane fills with 16-byte cp.async copies running ahead of it, in rounds:
+// wait for the copies of the round before, top the ring up, walk up to
+// IZG_IDXL_ROUND entries of what has landed.  All lanes of a warp wait at the
+// same instruction once per round, and every entry is read at shared-memory
+// latency.  (The first version loaded each entry from global memory with L1
+// prefetches ahead: 0.93 ms on 65,536 C5 pages, one exposed L2 / HBM latency
+// per entry since ~450 independent streams per SM thrash L1.)
+#ifndef IZG_IDXL_RING
+#define IZG_IDXL_RING 8  // 16-byte chunks per lane (0: the global-load walk)
+#endif
+#ifndef IZG_IDXL_ROUND
+#define IZG_IDXL_ROUND 2  // entries per round (65,536 C5 pages: 2 / 3 / 4 / 6 -> 0.49 / 0.54 / 0.52 / 0.60 ms)
+#endif
+#ifndef IZG_IDXL_PAIR
+#define IZG_IDXL_PAIR 1  // store records in pairs (whole sectors)
+#endif
+constexpr uint32_t kIdxRingChunks = IZG_IDXL_RING;
 struct IdxLaneLayout {
-  // per warp: running counts cnt[33][32], array sizes nn[33][32] (u32)
+  // per warp: running counts cnt[33][32], array sizes nn[33][32] (u32), then the lanes' rings
   static constexpr uint32_t kWarpBytes = 2 * 33 * 32 * 4;
-  static constexpr size_t kSmem = kIdxLaneWarps * kWarpBytes;
+  static constexpr uint32_t kRingOff = kIdxLaneWarps * kWarpBytes;
+  static constexpr size_t kSmem = kRingOff + kIdxLaneWarps * 32 * 16 * kIdxRingChunks;
 };
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 
 template <bool ARRAY, int ST>
 __global__ void __launch_bounds__(kIdxLaneWarps * 32)
@@ -319,6 +343,127 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
   uint32_t s = 0, packed = 1, k = 0;
   bool ovf = false;  // a cursor passed 65,535 (snapshot rows are 16-bit)
   uint4* snap = reinterpret_cast<uint4*>(ix.snap + (size_t)c * 512);
+#if IZG_IDXL_RING
+  {
+    constexpr uint32_t kRingBytes16 = 16u * kIdxRingChunks;
+    const uint32_t ring = smem_u32(smem) + IdxLaneLayout::kRingOff +
+                          (uint32_t)(warp * 32 + lane) * kRingBytes16;
+    const uintptr_t g0 = reinterpret_cast<uintptr_t>(ba) & ~uintptr_t(15);
+    const uint32_t phase = (uint32_t)(reinterpret_cast<uintptr_t>(ba) - g0);
+    const uint32_t nchunks = (phase + 4u * (uint32_t)ba_words + 15u) >> 4;  // covering the byte array
+    uint32_t pf = 0;      // next chunk to copy; chunks below it were issued
+    uint32_t pfprev = 0;  // `pf` one round ago
+    bool walking = true;
+    uint4 held = make_uint4(0, 0, 0, 0);  // an even block's record, stored with the next one
+    while (walking && k < nblocks) {
+      const uint32_t curc = (s + phase) >> 4;
+      // Two rounds of copies may be in flight.  Chunks below `pfprev` were issued two or
+      // more rounds ago: they are complete after wait_group 1.  When the walk has reached
+      // the last round's chunks (or a long entry skipped over them) wait for those too —
+      // always BEFORE issuing new copies: a late copy must not land on a newer chunk's slot,
+      // and the slots refilled below hold chunks under `curc`.
+      uint32_t landed = pfprev;
+      if (curc + 1 >= pfprev) {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        landed = pf;
+      } else {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      }
+      if (pf < curc) pf = landed = curc;  // a long entry jumped past the ring
+      pfprev = pf;
+      while (pf < curc + kIdxRingChunks && pf < nchunks) {
+        cp_async16(ring + 16u * (pf % kIdxRingChunks), reinterpret_cast<const void*>(g0 + 16u * pf));
+        ++pf;
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll 1
+      for (uint32_t step = 0; step < IZG_IDXL_ROUND && k < nblocks; ++step, ++k) {
+        if (s + 2 > Lc) {
+          wst = IZG_E_FP_TRUNC_META;
+          walking = false;
+          break;
+        }
+        const bool have3 = s + 2 < Lc;
+        if (((s + (have3 ? 2u : 1u) + phase) >> 4) >= landed) break;  // next round
+        const uint32_t o = s + phase;
+        const uint32_t b = lds8(ring + (o % kRingBytes16));
+        const uint32_t mb = lds8(ring + ((o + 1) % kRingBytes16));
+        const uint32_t c3 = have3 ? lds8(ring + ((o + 2) % kRingBytes16)) : 0u;
+#ifdef IZG_IDXL_DEBUG
+        if (b != ba[s] || mb != ba[s + 1])
+          printf("ring mismatch page %u k %u s %u o %u got %u %u want %u %u pf %u landed %u curc %u nch %u\n",
+                 c, k, s, o, b, mb, (uint32_t)ba[s], (uint32_t)ba[s + 1], pf, landed, curc, nchunks);
+#endif
+        walking = false;  // left false by every error exit of the step
+        do {
+      if (b > 32 || mb > 32 || b > mb) {
+        wst = IZG_E_FP_WIDTHS;
+        break;
+      }
+      uint32_t e = b, cc = 0, cur = 0;
+      if (mb > b) {
+        if (s + 2 >= Lc) {
+          wst = IZG_E_FP_TRUNC_META;
+          break;
+        }
+        cc = c3;
+        if (cc == 0) {
+          wst = IZG_E_FP_EMPTY_EXC;
+          break;
+        }
+        if (s + 3 + cc > Lc) {
+          wst = IZG_E_FP_TRUNC_POS;
+          break;
+        }
+        const uint32_t w = mb - b;
+        cur = cnt[w * 32 + lane];
+        cnt[w * 32 + lane] = cur + cc;
+        ovf |= cur + cc > 65535u;
+        e = b | w << 6 | cc << 12;
+        if (lst == IZG_OK && (uint64_t)cur + cc > nn[w * 32 + lane] && packed + 4 * b <= A)
+          lst = IZG_E_FP_EXHAUSTED;
+      }
+      if (lst == IZG_OK && packed + 4 * b > A) lst = IZG_E_FP_OVERRUN;
+#ifndef IZG_ABL_IDX_NOREC  // developer ablation (decode broken): no record stores
+#if IZG_IDXL_PAIR
+      // records leave two at a time: a whole 32-byte sector per pair
+      if (k & 1u) {
+        stg128_cg(rec + k - 1, held);
+        stg128_cg(rec + k, make_uint4(e, packed, s + 3, cur));
+      } else if (k + 1 == nblocks) {
+        stg128_cg(rec + k, make_uint4(e, packed, s + 3, cur));
+      } else {
+        held = make_uint4(e, packed, s + 3, cur);
+      }
+#else
+      stg128_cg(rec + k, make_uint4(e, packed, s + 3, cur));
+#endif
+#endif
+      packed += 4 * b;
+      s += cc ? 3 + cc : 2;
+      if ((k & 31u) == 31u || k + 1 == nblocks) {  // cursors after 32 (k / 32 + 1) blocks
+#pragma unroll
+        for (uint32_t w4 = 0; w4 < 4; ++w4) {
+          uint32_t x[4];
+#pragma unroll
+          for (uint32_t j = 0; j < 4; ++j) {
+            const uint32_t w = 8 * w4 + 2 * j + 1;  // widths w, w + 1 -> one word
+            x[j] = min(cnt[w * 32 + lane], 65535u) | min(cnt[(w + 1) * 32 + lane], 65535u) << 16;
+          }
+          stg128_cg(snap + (k >> 5) * 4 + w4, make_uint4(x[0], x[1], x[2], x[3]));
+        }
+      }
+          walking = true;
+        } while (false);
+        if (!walking) break;
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#if IZG_IDXL_PAIR
+    if (!walking && (k & 1u)) stg128_cg(rec + k - 1, held);  // the walk stopped on an odd block
+#endif
+  }
+#else
 #pragma unroll
   for (uint32_t a = 0; a < kIdxLaneAhead; a += 128)
     if (a < Lc) asm volatile("prefetch.global.L1 [%0];" ::"l"(ba + a));
@@ -341,7 +486,7 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
     const uint32_t* bw = reinterpret_cast<const uint32_t*>(ba) + (s >> 2);
     uint32_t x = ld_ca_u32(bw);
     if (s & 3) x = funnel_r(x, (s >> 2) + 1 < (Lc + 3) / 4 ? ld_ca_u32(bw + 1) : 0u, 8 * (s & 3));
-    const uint32_t b = x & 0xFFu, mb = (x >> 8) & 0xFFu;
+    const uint32_t b = x & 0xFFu, mb = (x >> 8) & 0xFFu, c3 = (x >> 16) & 0xFFu;
     if (b > 32 || mb > 32 || b > mb) {
       wst = IZG_E_FP_WIDTHS;
       break;
@@ -352,7 +497,7 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
         wst = IZG_E_FP_TRUNC_META;
         break;
       }
-      cc = (x >> 16) & 0xFFu;
+      cc = c3;
       if (cc == 0) {
         wst = IZG_E_FP_EMPTY_EXC;
         break;
@@ -388,6 +533,7 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
       }
     }
   }
+#endif
   int32_t st = wst;
   if (st == IZG_OK && s != L) st = IZG_E_FP_BA_LEN;
   const bool dir_ok = st == IZG_OK && dst == IZG_OK;  // fp_index_kernel reports `end` only then

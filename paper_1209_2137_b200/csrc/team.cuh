@@ -885,7 +885,11 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
       if (!live) e.x = 0;
       const uint32_t myb = e.x & 63u, myw = (e.x >> 6) & 63u, myc = e.x >> 12;
       const uint32_t myoff = e.y, mybp = e.z, mycur = e.w;
+#ifdef IZG_ABL_TEAM_NOPATCH  // developer ablation (wrong output): no exception path
+      const bool tot = false;
+#else
       const bool tot = __any_sync(0xFFFFFFFFu, myc != 0);
+#endif
       uint32_t v[4][4];
       if (pal) {
 #if IZG_TEAM_NARROW
@@ -913,7 +917,11 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_s(sb + LY::kEmpty + 8u * slot);  // done with the staging
+#ifdef IZG_ABL_TEAM_NOSCAN  // developer ablation (wrong output): no prefix sum, no carry chain
+      if (false) {
+#else
       if (kArray) {
+#endif
         uint4 ex, incl;
         uint32_t q3[4] = {0, 0, 0, 0};
         team_scan_local<DELTA>(v, ex, incl, q3, lane);
@@ -941,6 +949,11 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
         }
         team_scan_apply<DELTA>(v, u4add(pv, ex), q3);
       }
+#ifdef IZG_ABL_TEAM_NOSTORE  // developer ablation (no output): nothing stored
+      if (v[0][0] == 0xFFFFFFFFu && v[3][3] == 0x12345678u && v[1][2] == 77u) bad = true;
+      if (true) {
+      } else
+#endif
       if (orow >= 0 && blk0 + 4 <= nb) {
         if (!tot) tile.wait_free();
         tile.write(v);
