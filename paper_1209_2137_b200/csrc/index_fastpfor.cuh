@@ -240,6 +240,9 @@ constexpr uint32_t kIdxLaneAhead = IZG_IDXL_AHEAD;  // bytes the L1 prefetches r
 #ifndef IZG_IDXL_ROUND
 #define IZG_IDXL_ROUND 2  // entries per round (65,536 C5 pages: 2 / 3 / 4 / 6 -> 0.49 / 0.54 / 0.52 / 0.60 ms)
 #endif
+#ifndef IZG_IDXL_DEPTH
+#define IZG_IDXL_DEPTH 2  // rounds of copies in flight
+#endif
 #ifndef IZG_IDXL_PAIR
 #define IZG_IDXL_PAIR 1  // store records in pairs (whole sectors)
 #endif
@@ -351,30 +354,36 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
     const uintptr_t g0 = reinterpret_cast<uintptr_t>(ba) & ~uintptr_t(15);
     const uint32_t phase = (uint32_t)(reinterpret_cast<uintptr_t>(ba) - g0);
     const uint32_t nchunks = (phase + 4u * (uint32_t)ba_words + 15u) >> 4;  // covering the byte array
-    uint32_t pf = 0;      // next chunk to copy; chunks below it were issued
-    uint32_t pfprev = 0;  // `pf` one round ago
+    uint32_t pf = 0;  // next chunk to copy; chunks below it were issued
+    uint32_t pfh[IZG_IDXL_DEPTH];  // `pf` after the issue of each of the last rounds, newest first
+#pragma unroll
+    for (int i = 0; i < IZG_IDXL_DEPTH; ++i) pfh[i] = 0;
     bool walking = true;
     uint4 held = make_uint4(0, 0, 0, 0);  // an even block's record, stored with the next one
     while (walking && k < nblocks) {
       const uint32_t curc = (s + phase) >> 4;
-      // Two rounds of copies may be in flight.  Chunks below `pfprev` were issued two or
-      // more rounds ago: they are complete after wait_group 1.  When the walk has reached
-      // the last round's chunks (or a long entry skipped over them) wait for those too —
-      // always BEFORE issuing new copies: a late copy must not land on a newer chunk's slot,
-      // and the slots refilled below hold chunks under `curc`.
-      uint32_t landed = pfprev;
-      if (curc + 1 >= pfprev) {
+      // Up to IZG_IDXL_DEPTH rounds of copies are in flight.  Chunks below pfh[DEPTH-1]
+      // were issued DEPTH or more rounds ago: complete after wait_group DEPTH-1.  When the
+      // walk has reached younger chunks (or a long entry skipped over them) wait for
+      // everything — always BEFORE issuing new copies: a late copy must not land on a newer
+      // chunk's slot, and the slots refilled below hold chunks under `curc`.
+      uint32_t landed = pfh[IZG_IDXL_DEPTH - 1];
+      if (curc + 1 >= landed) {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
+        if (pf < curc) pf = curc;  // a long entry jumped past the ring
         landed = pf;
+#pragma unroll
+        for (int i = 0; i < IZG_IDXL_DEPTH; ++i) pfh[i] = pf;
       } else {
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(IZG_IDXL_DEPTH - 1) : "memory");
       }
-      if (pf < curc) pf = landed = curc;  // a long entry jumped past the ring
-      pfprev = pf;
       while (pf < curc + kIdxRingChunks && pf < nchunks) {
         cp_async16(ring + 16u * (pf % kIdxRingChunks), reinterpret_cast<const void*>(g0 + 16u * pf));
         ++pf;
       }
+#pragma unroll
+      for (int i = IZG_IDXL_DEPTH - 1; i > 0; --i) pfh[i] = pfh[i - 1];
+      pfh[0] = pf;
       asm volatile("cp.async.commit_group;" ::: "memory");
 #pragma unroll 1
       for (uint32_t step = 0; step < IZG_IDXL_ROUND && k < nblocks; ++step, ++k) {
