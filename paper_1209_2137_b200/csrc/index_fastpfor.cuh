@@ -208,8 +208,9 @@ __global__ void __launch_bounds__(kIdxWarps * 32)
 // byte-array walk is a serial loop of a handful of instructions per entry
 // (codec_patched.cpp:309-336, every check in the reference's order), so a
 // warp walks 32 pages at once and the pass costs a few instructions per 512
-// integers; its time is the memory latency of the 32 walks, hidden by the
-// warps resident on the SM.  The exception directory (:338-379) is read
+// integers; its time is the latency of the walks (every page's walk runs at
+// once), which is why the byte array is read from per-lane rings in shared
+// memory filled by cp.async copies ahead of the walk (below).  The exception directory (:338-379) is read
 // first (its errors still rank after the walk's, as in the reference); each
 // block's cursor in its width array is a running count per width, kept per
 // lane in shared memory ([width][lane]: conflict-free); the block loop's

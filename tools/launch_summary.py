@@ -21,8 +21,8 @@ for r in rows[1:]:
     unit = r[h.index("Metric Unit")]
     us = v / 1e3 if unit in ("ns", "nsecond") else v if unit in ("us", "usecond") else v * 1e3
     dur[name].append(us)
-# the step's launches are the long ones (>= 0.5 ms at C5; the lane index pass takes 0.9 ms)
-step = {k: [x for x in v if x >= 500.0] for k, v in dur.items()}
+# the step's launches are the long ones (>= 0.3 ms at C5; the lane index pass takes 0.5 ms)
+step = {k: [x for x in v if x >= 300.0] for k, v in dur.items()}
 tot = sum(sum(v) / len(v) for v in step.values() if v)
 for k, v in step.items():
     if v:
