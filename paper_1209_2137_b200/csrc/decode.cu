@@ -116,24 +116,6 @@ int team_threads();
 #ifndef IZG_TEAM_MIN
 #define IZG_TEAM_MIN 128
 #endif
-// SIMD-BP128 team decode (team_bp.cuh: one CTA of 8 decoding warps + a
-// staging warp per chunk): decode_team.cu.  IZG_BPTEAM=0 / 1 forces it.
-using BpTeamFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
-                          uint32_t*, uint32_t*, const CUtensorMap, int);
-BpTeamFn pick_bp_team(int delta);
-size_t bp_team_smem_bytes();
-#ifndef IZG_BPTEAM_MIN
-#define IZG_BPTEAM_MIN 0xFFFFFFFFu
-#endif
-#ifndef IZG_BPTEAM_MAX
-#define IZG_BPTEAM_MAX 0u
-#endif
-int env_switch(const char* name);
-bool bp_team_wanted(uint32_t n_chunks) {
-  static const int force = env_switch("IZG_BPTEAM");
-  if (force >= 0) return force != 0;
-  return n_chunks >= IZG_BPTEAM_MIN && n_chunks <= IZG_BPTEAM_MAX;
-}
 int env_switch(const char* name) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : -1;
@@ -245,7 +227,7 @@ struct DeviceInfo {
   int sms = 0;
   // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink,
   //  + 3 kCodecs: split kernels, 4 kCodecs + 0..2: group kernels KW = 2, 4, 8)][delta]
-  int occ[4 * kCodecs + 7][5] = {};  // + 4 kCodecs + 3: big indexed, + 4: CTA kernel, + 5: team, + 6: BP team
+  int occ[4 * kCodecs + 6][5] = {};  // + 4 kCodecs + 3: big indexed, + 4: CTA kernel, + 5: team
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -393,24 +375,6 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                    delta, kfn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;
-  if (!probe && codec == IZG_SIMDBP128 && bp_team_wanted(n_chunks)) {
-    BpTeamFn bfn = pick_bp_team(delta);
-    int bper_sm = 0, bsms = 0;
-    uint32_t* bcounter = nullptr;
-    rc = prepare(dev, 4 * kCodecs + 6, delta, reinterpret_cast<const void*>(bfn), team_threads(),
-                 bp_team_smem_bytes(), &bper_sm, &bsms, &bcounter);
-    if (rc != IZG_SUCCESS) return rc;
-    cudaStream_t bs = static_cast<cudaStream_t>(stream);
-    if (cudaMemsetAsync(bcounter, 0, sizeof(uint32_t), bs) != cudaSuccess) return IZG_ERR_CUDA;
-    const uint32_t grid = (uint32_t)std::min<uint64_t>(n_chunks, (uint64_t)bper_sm * bsms);
-    CUtensorMap omap;
-    std::memset(&omap, 0, sizeof(omap));
-    const int tma_out = IZG_TMA_STORE && make_out_map(&omap, d_out) ? 1 : 0;
-    bfn<<<grid, team_threads(), bp_team_smem_bytes(), bs>>>(d_words, d_chunks, n_chunks, d_out,
-                                                            d_status, d_consumed, bcounter, omap,
-                                                            tma_out);
-    return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
-  }
   if (!probe && cta_wanted(codec, delta, n_chunks)) {
     GroupFn cfn = pick_cta(delta);
     int cper_sm = 0, csms = 0;

@@ -2,7 +2,6 @@
 // team.cuh (one CTA of 8 warps per page, shared TMA staging, windowed bulk
 // unpack of the exception arrays, two-level prefix sum).
 #include "team.cuh"
-#include "team_bp.cuh"
 
 namespace izg {
 
@@ -19,21 +18,6 @@ TeamFn pick_team(int delta) {
   }
   return nullptr;
 }
-
-using BpTeamFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*, int32_t*,
-                          uint32_t*, uint32_t*, const CUtensorMap, int);
-
-BpTeamFn pick_bp_team(int delta) {
-  switch (delta) {
-    case IZG_DELTA_NONE: return bp_team_kernel<IZG_DELTA_NONE>;
-    case IZG_DELTA_D1: return bp_team_kernel<IZG_DELTA_D1>;
-    case IZG_DELTA_D4: return bp_team_kernel<IZG_DELTA_D4>;
-    case IZG_DELTA_D2: return bp_team_kernel<IZG_DELTA_D2>;
-    case IZG_DELTA_DM: return bp_team_kernel<IZG_DELTA_DM>;
-  }
-  return nullptr;
-}
-size_t bp_team_smem_bytes() { return BpTeamLayout::kSmem; }
 
 size_t team_smem_bytes() { return TeamLayout::kSmem; }
 int team_threads() { return kTeamThreads; }
