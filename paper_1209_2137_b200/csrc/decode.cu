@@ -2,7 +2,7 @@
 //
 // Kernel shape: persistent CTAs of kWarps independent warps.
 // Each warp claims whole chunks, streams the chunk's compressed payload into
-// its private 8 KiB shared-memory ring with TMA bulk copies (cp.async.bulk +
+// its private 4 KiB shared-memory ring with TMA bulk copies (cp.async.bulk +
 // mbarrier complete_tx), decodes straight out of the ring with the prefix sum
 // fused, and writes every decoded integer to HBM exactly once.
 #include <cuda.h>

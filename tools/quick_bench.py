@@ -5,6 +5,12 @@ import numpy as np, torch
 import harness as H
 import paper_1209_2137_b200 as P
 
+try:  # the driver-measured copy bandwidth (roofline denominator)
+    PEAK = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                             "MEASURED_PEAKS.json")))["hbm_gbs"])
+except Exception:
+    PEAK = 6532.9
+
 def run(name, model, count, d, seed=1, rate=0, reps=20, raw=False):
     codec = P.make_codec(name)
     t0 = time.time()
@@ -34,7 +40,7 @@ def run(name, model, count, d, seed=1, rate=0, reps=20, raw=False):
     gb = b.algorithmic_bytes / t / 1e9
     print(json.dumps(dict(name=name, model=model, d=d, rate=rate, raw=raw, ok=bool(ok),
         bits_per_int=round(32 * b.payload_words / n, 3), ms=round(t * 1e3, 4),
-        gints=round(n / t / 1e9, 2), alg_GBps=round(gb, 1), frac=round(gb / 6532.9, 3),
+        gints=round(n / t / 1e9, 2), alg_GBps=round(gb, 1), frac=round(gb / PEAK, 3),
         prep_s=round(t1 - t0, 1))), flush=True)
 
 if __name__ == "__main__":
