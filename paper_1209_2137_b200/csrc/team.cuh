@@ -71,9 +71,6 @@ constexpr uint32_t kTeamXb = IZG_TEAM_XB;     // packed exception arrays of a wi
 #ifndef IZG_TEAM_IDLE_NS
 #define IZG_TEAM_IDLE_NS 64  // staging warp: sleep after a pass without progress
 #endif
-#ifndef IZG_TEAM_AHEAD
-#define IZG_TEAM_AHEAD 2  // warp 0 stages more once fewer than this many lie ahead
-#endif
 #ifndef IZG_TEAM_MINCTAS
 #define IZG_TEAM_MINCTAS 3  // CTAs per SM the register allocation allows for
 #endif
