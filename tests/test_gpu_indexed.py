@@ -268,6 +268,48 @@ def test_lane_index_pass(env):
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
 
 
+_LARGE = r'''
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import harness as H
+import paper_1209_2137_b200 as P
+from paper_1209_2137_b200.device import host_checksum
+codec = P.make_codec("simdfastpfor-s4")
+for model, count, d, rate in [("cluster", 8192, (20, 29), 0), ("geometric", 2048, 32, 100000)]:
+    vals, _ = H.gen_arrays(model, count, 65536, d, seed=11, rate_ppm=rate)
+    flat = vals.reshape(-1)
+    enc = H.encode_chunks(codec, flat, np.arange(count, dtype=np.uint64) * 65536,
+                          np.full(count, 65536, np.uint32), allow_wrap=model == "geometric")
+    want = host_checksum(flat)
+    b = P.DeviceBatch(codec, enc)
+    for _ in range(4):   # the failure this guards against depended on memory load
+        b.out.zero_()
+        b.decode()
+        torch.cuda.synchronize()
+        b.check()
+        assert b.checksum() == want
+print("ok")
+'''
+
+
+@pytest.mark.parametrize("team", ["0", "1"], ids=["warp-per-page", "team"])
+def test_lane_index_pass_large_batch(cuda, team):
+    """The lane-per-page index pass on batches large enough to load the memory
+    system (8,192 C5 pages, 2,048 C4 pages at 10 % outliers): its cp.async
+    rings once let a late copy land on a refilled slot, which only showed
+    under load.  Device checksum against the generated arrays, repeatedly."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IZG_INDEX_LANES_MIN="0", IZG_SPLIT="0", IZG_TEAM=team)
+    r = subprocess.run([sys.executable, "-c", _LARGE.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-1000:] + r.stderr[-3000:]
+
+
 @pytest.mark.parametrize("name", ["simdfastpfor-s4", "simdfastpfor", "simdbp128-s4"])
 def test_decode_phases_equal_one_call(cuda, name):
     """izg_decode_ws_phase: the page index pass (phase 1) on a side stream,
