@@ -146,6 +146,18 @@ def test_team_kernel_heavy_pages(cuda, lanes):
          _HEAVY.format(root=ROOT))
 
 
+@pytest.mark.parametrize("lanes", ["0", "1000000000"], ids=["lane-index", "warp-index"])
+def test_team_kernel_random_batches(cuda, lanes):
+    """tools/team_stress.py for 15 s: random batch sizes, ragged lengths with
+    VByte remainders, data models, outlier rates and delta modes, every batch
+    decoded three times and compared with the generated arrays word for word
+    (a 10-minute run of the same tool covered 835,000 arrays)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "team_stress.py"), "15", "7"],
+                       cwd=ROOT, env=dict(os.environ, IZG_TEAM="1", IZG_INDEX_LANES_MIN=lanes),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().startswith("ok"), r.stdout[-1000:] + r.stderr[-3000:]
+
+
 def test_team_kernel_config_shapes(cuda, ref):
     _run({"IZG_TEAM": "1", "IZG_SPLIT": "0"},
          f"import sys; sys.path.insert(0, {ROOT!r}); from tests.config_cases import main; main()")
