@@ -694,3 +694,16 @@ extern "C" int izg_encode(int codec, int delta, const uint32_t* d_values, izg_ch
   fn<<<grid, kEncWarps * 32, esmem, s>>>(d_values, d_chunks, n_chunks, d_words, d_status, counter);
   return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
 }
+
+#ifdef IZG_BOUNDS
+// Bounds-check build: this translation unit's counters (the page index kernels).
+extern "C" int izg_debug_bounds_index(void* host, int reset) {
+  if (cudaMemcpyFromSymbol(host, izg::g_izg_oob, sizeof(izg::g_izg_oob)) != cudaSuccess) return -1;
+  if (reset) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, izg::g_izg_oob) != cudaSuccess) return -1;
+    cudaMemset(p, 0, sizeof(izg::g_izg_oob));
+  }
+  return 0;
+}
+#endif

@@ -360,7 +360,10 @@ template <int ST>
 __device__ __forceinline__ bool fp_patch_lean(uint32_t t, const uint32_t* page,
                                               const uint8_t* ba, uint32_t myb, uint32_t myw,
                                               uint32_t myc, uint32_t mybp, uint32_t mycur,
-                                              uint32_t mybase, int lane) {
+                                              uint32_t mybase, int lane, uint32_t nw = 0,
+                                              uint32_t chunk = 0) {
+  (void)nw;
+  (void)chunk;
   const uint32_t q = (lane >> 3) & 3u, s8 = lane & 7;
   uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));
   mxc = max(mxc, __shfl_xor_sync(0xFFFFFFFFu, mxc, 16));
@@ -389,6 +392,12 @@ __device__ __forceinline__ bool fp_patch_lean(uint32_t t, const uint32_t* page,
         sh[j] = bit & 31u;
         step = 1u;
       }
+      IZG_CHECK(!nw || !ok[j] || izg_in_span(reinterpret_cast<uintptr_t>(pb + e), 1, page, nw), 6,
+                chunk, e);
+      IZG_CHECK(!nw || (izg_in_span(reinterpret_cast<uintptr_t>(arr + word), 4, page, nw) &&
+                        izg_in_span(reinterpret_cast<uintptr_t>(
+                                        arr + word + (sh[j] + myw > 32 ? step : 0u)), 4, page, nw)),
+                7, chunk, word);
       pp[j] = ok[j] ? ld_u8(pb + e) : 0u;
       lo[j] = ld_u32(arr + word);
       hi[j] = ld_u32(arr + word + (sh[j] + myw > 32 ? step : 0u));
@@ -414,9 +423,10 @@ __device__ __forceinline__ bool fp_patch_lean(uint32_t t, const uint32_t* page,
 template <int ST>
 __device__ __forceinline__ bool fp_patch(uint32_t t, const uint32_t* page, const uint8_t* ba,
                                          uint32_t myb, uint32_t myw, uint32_t myc, uint32_t mybp,
-                                         uint32_t mycur, uint32_t mybase, int lane) {
+                                         uint32_t mycur, uint32_t mybase, int lane, uint32_t nw = 0,
+                                         uint32_t chunk = 0) {
 #if IZG_PATCH_LEAN
-  return fp_patch_lean<ST>(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane);
+  return fp_patch_lean<ST>(t, page, ba, myb, myw, myc, mybp, mycur, mybase, lane, nw, chunk);
 #endif
   const uint32_t q = (lane >> 3) & 3u, s8 = lane & 7;
   uint32_t mxc = max(myc, __shfl_xor_sync(0xFFFFFFFFu, myc, 8));

@@ -35,3 +35,16 @@ extern "C" int izg_debug_team_prof(void* host, int reset) {
   return 0;
 }
 #endif
+
+#ifdef IZG_BOUNDS
+// {violations, kind of the first, its chunk, its offset}; reset != 0 clears the counters.
+extern "C" int izg_debug_bounds(void* host, int reset) {
+  if (cudaMemcpyFromSymbol(host, izg::g_izg_oob, sizeof(izg::g_izg_oob)) != cudaSuccess) return -1;
+  if (reset) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, izg::g_izg_oob) != cudaSuccess) return -1;
+    cudaMemset(p, 0, sizeof(izg::g_izg_oob));
+  }
+  return 0;
+}
+#endif

@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(kIdxLaneWarps * 32)
         asm volatile("cp.async.wait_group %0;" ::"n"(IZG_IDXL_DEPTH - 1) : "memory");
       }
       while (pf < curc + kIdxRingChunks && pf < nchunks) {
+        IZG_CHECK(izg_in_span(g0 + 16u * pf, 16, page, nw), 8, c, pf);
         cp_async16(ring + 16u * (pf % kIdxRingChunks), reinterpret_cast<const void*>(g0 + 16u * pf));
         ++pf;
       }

@@ -23,6 +23,30 @@
 
 namespace izg {
 
+// IZG_BOUNDS (developer build; the pool refuses compute-sanitizer): every
+// global access range the team decode and the lane index pass form is checked against the
+// chunk's own span — reads inside the 16-byte-aligned cover of [page, page + n_words),
+// writes inside [out + out_off, + n) — and violations are counted (izg_debug_bounds).
+#ifdef IZG_BOUNDS
+__device__ unsigned int g_izg_oob[4];  // count, kind of the first, its chunk, its offset
+__device__ __forceinline__ void izg_check(bool ok, uint32_t kind, uint32_t chunk, uint32_t off) {
+  if (!ok && atomicAdd(&g_izg_oob[0], 1u) == 0) {
+    g_izg_oob[1] = kind;
+    g_izg_oob[2] = chunk;
+    g_izg_oob[3] = off;
+  }
+}
+// [a, a + len) inside the 16-byte-aligned cover of [page, page + 4 nw)
+__device__ __forceinline__ bool izg_in_span(uintptr_t a, uint64_t len, const void* page, uint32_t nw) {
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(page) & ~uintptr_t(15);
+  const uintptr_t hi = (reinterpret_cast<uintptr_t>(page) + 4ull * nw + 15) & ~uintptr_t(15);
+  return a >= lo && a + len <= hi;
+}
+#define IZG_CHECK(ok, kind, chunk, off) izg_check((ok), (kind), (chunk), (off))
+#else
+#define IZG_CHECK(ok, kind, chunk, off)
+#endif
+
 constexpr uint32_t kSB = 1024;                // bytes per ring stage
 constexpr uint32_t kNS = 4;                   // stages per warp ring
 constexpr uint32_t kRingBytes = kSB * kNS;    // 4 KiB per warp

@@ -477,7 +477,7 @@ __device__ __forceinline__ uint32_t team_place(uint32_t head, uint32_t tail, uin
 // `ctx` = the page's context (bounds P at +0, S at +80).  Lane 0 only.
 __device__ __forceinline__ bool team_issue(TeamProducer& pr, uint32_t sb, uint32_t ctx, uint32_t j,
                                            uint32_t nb, const uint32_t* page, const uint8_t* ba,
-                                           const uint4* rec) {
+                                           const uint4* rec, uint32_t nw, uint32_t c) {
   using LY = TeamLayout;
   const uint32_t P0 = lds32(ctx + 4u * j), P1 = lds32(ctx + 4u * j + 4u);
   const uint32_t S0 = lds32(ctx + 80u + 4u * j), S1 = lds32(ctx + 84u + 4u * j);
@@ -489,6 +489,14 @@ __device__ __forceinline__ bool team_issue(TeamProducer& pr, uint32_t sb, uint32
   uint32_t lens = S1 > S0 ? (uint32_t)(gs1 - gs0) : 0u;
   const bool pskip = lens > kTeamPs;
   if (pskip) lens = 0;
+#ifdef IZG_BOUNDS_SELFTEST  // the checker must fire: pretend the chunk is half as long
+  IZG_CHECK(izg_in_span(gp0, lenp, page, nw / 2), 1, c, P0);
+#else
+  IZG_CHECK(izg_in_span(gp0, lenp, page, nw), 1, c, P0);
+#endif
+  IZG_CHECK(pskip || izg_in_span(gs0, lens, page, nw), 2, c, S0);
+  (void)nw;
+  (void)c;
   uint32_t tp = 0xFFFFFFFFu, ts = 0xFFFFFFFFu;
   if (pr.gi != pr.gd) {  // oldest unread super-iteration: gd
     const uint2 al = lds64(sb + LY::kAlloc + 8u * (pr.gd % kTeamSlots));
@@ -607,7 +615,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
       return c;
     };
     // context scalars (u32 index from +288): 0 c, 1 nb, 2 K, 3 A, 4 flags (1 ovf, 2 exception rows
-    // aligned), 5..6 word_off
+    // aligned), 5..6 word_off, 7 n_words
     constexpr uint32_t kScal = 288, kSnapOff = (20 + 20 + 32 + 24) * 4;
     uint32_t c_next = claim();
     uint32_t pprep = 0;   // decodable pages prepared so far (contexts / descriptors written)
@@ -681,7 +689,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
               prefetch_l2(page + h.y, 4u * (h.z - h.y));  // exception arrays
               sts128(ctx + kScal, c, nb, K, A);
               sts128(ctx + kScal + 16, (ovf ? 1u : 0u) | (xal ? 2u : 0u), (uint32_t)ch.word_off,
-                     (uint32_t)(ch.word_off >> 32), 0);
+                     (uint32_t)(ch.word_off >> 32), ch.n_words);
             }
             if (pprep >= 2) mbar_wait_s(sb + LY::kPfree + 8u * pp, ((pprep >> 1) - 1u) & 1u);
             sts32(sb + LY::kDirb + 4u * (36u * pp + lane + 1), dirv);
@@ -714,7 +722,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
           const uint32_t* page = words + ((uint64_t)sc2.z << 32 | sc2.y);
           const uint8_t* ba = reinterpret_cast<const uint8_t*>(page + sc.w + 1);
           while (ka < sc.z && pr.gi < pr.gd + kTeamSlots) {
-            if (!team_issue(pr, sb, ctx, ka, sc.y, page, ba, ix.page_rec(sc.x))) break;
+            if (!team_issue(pr, sb, ctx, ka, sc.y, page, ba, ix.page_rec(sc.x), sc2.w, sc.x)) break;
             ++pr.gi;
             ++ka;
             r |= 1u;
@@ -789,6 +797,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
               mbar_arrive_expect_tx_s(bar, sum);
             }
             __syncwarp();
+            IZG_CHECK(!g || izg_in_span(s0, len, page, sc2.w), 3, sc.x, lane);
             if (g) bulk_g2s_s(dst, reinterpret_cast<const void*>(s0), len, bar, pr.policy);
           } else {
             if (lane == 0) {
@@ -907,7 +916,7 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
           bad |= team_patch(tile.t, info.y + mybp, xr.x, mycur - xr.y, myw, myb, myc, lane);
         } else {
           bad |= fp_patch<kVertical>(tile.t, page, ba, myb, myw, myc, mybp, mycur,
-                                     lds32(sb + LY::kDirb + 4u * (36u * pp + myw)), lane);
+                                     lds32(sb + LY::kDirb + 4u * (36u * pp + myw)), lane, ch.n_words, c);
         }
         __syncwarp();
         tile.read(v);
@@ -952,11 +961,13 @@ __global__ void __launch_bounds__(IZG_TEAM_LB_THREADS, IZG_TEAM_MINCTAS)
       } else
 #endif
       if (orow >= 0 && blk0 + 4 <= nb) {
+        IZG_CHECK(128u * (blk0 + 4) <= ch.n, 4, c, blk0);
         if (!tot) tile.wait_free();
         tile.write(v);
         tile.store((uint32_t)(orow + 4 * (int64_t)blk0));
       } else {
         __syncwarp();
+        IZG_CHECK(!live || 128u * (blk0 + q) + 16u * s8 + 16u <= ch.n, 5, c, blk0);
         if (live) store_direct(v, o + (size_t)(blk0 + q) * 128 + 16 * s8, oal);
       }
     }
