@@ -22,7 +22,7 @@ LIB = os.path.join(LIBDIR, "libintzip_b200.so")
 OBJDIR = os.path.join(LIBDIR, "obj")
 
 SOURCES = ["decode.cu", "decode_scalar.cu", "decode_probe.cu", "decode_split.cu",
-           "decode_group.cu", "decode_cta.cu", "decode_team.cu", "intersect.cu", "host.cpp", "container.cpp"]
+           "decode_group.cu", "decode_cta.cu", "decode_team.cu", "decode_relay.cu", "intersect.cu", "host.cpp", "container.cpp"]
 # per-source extra flags (none: decode_scalar.cu is built at -O3 again since
 # round 2, see the comment at its top); IZG_SCALAR_O1=1 restores the old
 # -Xptxas -O1 build of it for comparisons

@@ -18,6 +18,7 @@
 #include "decode_kernel.cuh"
 #include "group.cuh"
 #include "split.cuh"
+#include "relay.cuh"
 #include "encode.cuh"
 
 namespace izg {
@@ -95,6 +96,7 @@ using GroupFn = void (*)(const uint32_t*, const izg_chunk*, uint32_t, uint32_t*,
 GroupFn pick_group(int kw, int delta);
 // CTA-cooperative SIMD-BP128 kernels (one CTA per SM): decode_cta.cu.
 GroupFn pick_cta(int delta);
+RelayFn pick_relay(int delta);
 size_t cta_smem_bytes();
 int cta_threads();
 // Team SIMD-FastPFOR decode (one CTA per page, indexed path): decode_team.cu.
@@ -206,11 +208,42 @@ bool split_wanted(int codec, uint32_t n_chunks) {
   if (force >= 0) return force != 0;
   return n_chunks <= (codec == IZG_SIMDBP128 ? kSplitMaxChunksBp : kSplitMaxChunksFp);
 }
+// SIMD-BP128 batches of one to a few waves of the 3,552 resident warp slots
+// (BASELINE's C2 / C3: 4,096 chunks) take the relay kernel (relay.cuh) when
+// the caller gives a workspace: segments of a chunk claimed level by level,
+// so the batch's tail is quantised in segments instead of whole chunks.
+// IZG_RELAY=0 / 1 forces it off / on; IZG_RELAY_SEGS=1..32 (a power of two) sets the levels.
+#ifndef IZG_RELAY_MIN
+#define IZG_RELAY_MIN 2432
+#endif
+#ifndef IZG_RELAY_MAX
+#define IZG_RELAY_MAX 14208
+#endif
+// Measured (tools/relay_sweep.py, SIMD-BP128+D4, ClusterData d=29, ms, one warp per chunk
+// vs relay with 2 / 4 / 8 / 16 levels): 3,552 chunks 0.250 vs 0.247 / 0.239 / 0.232 / 0.241;
+// 4,096: 0.297 vs 0.269 / 0.265 / 0.261 / 0.273; 6,144: 0.397 vs 0.388 / 0.386 / 0.380 / 0.400;
+// 8,192: 0.510 vs 0.511 / 0.499 / 0.503 / 0.531; 12,288: 0.768 vs 0.747 / 0.732 / 0.744 /
+// 0.793; 16,384: 0.967 vs 0.970 / 0.969 / 0.985 / 1.051 — eight levels up to 7,168 chunks,
+// four above, none past four waves.  Below one wave (relay 8 vs one warp per chunk): 1,700
+// chunks 0.163 vs 0.150; 2,048: 0.175 vs 0.152; 2,560: 0.192 vs 0.203; 3,072: 0.206 vs 0.227;
+// 3,400: 0.228 vs 0.242 — from 2,432 chunks on.
+#ifndef IZG_RELAY_SPLIT8
+#define IZG_RELAY_SPLIT8 7168
+#endif
+bool relay_wanted(int codec, uint32_t n_chunks) {
+  if (codec != IZG_SIMDBP128) return false;
+  static const int force = env_switch("IZG_RELAY");
+  if (force >= 0) return force != 0;
+  return n_chunks >= IZG_RELAY_MIN && n_chunks <= IZG_RELAY_MAX;
+}
+uint64_t relay_ws_bytes(uint32_t n_chunks) { return relay_state_bytes(n_chunks) + 64; }
 uint64_t split_ws_offset(int codec, uint32_t n_chunks) {
   return codec == IZG_SIMDFASTPFOR ? (idx_workspace_bytes(n_chunks) + 15) / 16 * 16 : 0;
 }
 uint64_t workspace_bytes(int codec, uint32_t n_chunks) {
   const uint64_t base = codec == IZG_SIMDFASTPFOR ? idx_workspace_bytes(n_chunks) : 0;
+  if (relay_wanted(codec, n_chunks) && !split_wanted(codec, n_chunks))
+    return relay_ws_bytes(n_chunks);
   if (!split_wanted(codec, n_chunks)) return base;
   return split_ws_offset(codec, n_chunks) + split_state_bytes(n_chunks);
 }
@@ -227,7 +260,7 @@ struct DeviceInfo {
   int sms = 0;
   // [codec (+ kCodecs: indexed page path, + 2 kCodecs: probe sink,
   //  + 3 kCodecs: split kernels, 4 kCodecs + 0..2: group kernels KW = 2, 4, 8)][delta]
-  int occ[4 * kCodecs + 6][5] = {};  // + 4 kCodecs + 3: big indexed, + 4: CTA kernel, + 5: team
+  int occ[4 * kCodecs + 7][5] = {};  // + 4 kCodecs + 3: big indexed, + 4: CTA kernel, + 5: team, + 6: relay
   uint32_t* counters = nullptr;  // chunk-claim counters, one per in-flight launch
   uint32_t next_slot = 0;
 };
@@ -375,7 +408,10 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
                    delta, kfn, warps * 32, smem, &per_sm, &sms,
                    &counter);
   if (rc != IZG_SUCCESS) return rc;
-  if (!probe && cta_wanted(codec, delta, n_chunks)) {
+  const bool relay = !probe && !split && relay_wanted(codec, n_chunks) && d_ws &&
+                     (reinterpret_cast<uintptr_t>(d_ws) & 15) == 0 &&
+                     ws_bytes >= relay_ws_bytes(n_chunks);
+  if (!probe && !relay && cta_wanted(codec, delta, n_chunks)) {
     GroupFn cfn = pick_cta(delta);
     int cper_sm = 0, csms = 0;
     uint32_t* ccounter = nullptr;
@@ -391,6 +427,38 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     cfn<<<grid, cta_threads(), cta_smem_bytes(), cs>>>(d_words, d_chunks, n_chunks, d_out,
                                                        d_status, d_consumed, ccounter, omap,
                                                        tma_out);
+    return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
+  }
+  if (relay) {
+    RelayFn rfn = pick_relay(delta);
+    int rper_sm = 0, rsms = 0;
+    uint32_t* rcounter = nullptr;
+    rc = prepare(dev, 4 * kCodecs + 6, delta, reinterpret_cast<const void*>(rfn), warps * 32,
+                 smem, &rper_sm, &rsms, &rcounter);
+    if (rc != IZG_SUCCESS) return rc;
+    cudaStream_t rs = static_cast<cudaStream_t>(stream);
+    // per-chunk states and, behind them, the task counter: one memset
+    if (cudaMemsetAsync(d_ws, 0, relay_ws_bytes(n_chunks), rs) != cudaSuccess)
+      return IZG_ERR_CUDA;
+    static const int force_segs = [] {
+      const char* e = std::getenv("IZG_RELAY_SEGS");
+      const int v = e ? std::atoi(e) : 0;
+      return v >= 1 && v <= 32 && (v & (v - 1)) == 0 ? v : 0;
+    }();
+    RelayArgs ra;
+    ra.st = static_cast<RelayState*>(d_ws);
+    ra.next_task = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) +
+                                               relay_state_bytes(n_chunks));
+    ra.levels = (uint32_t)(force_segs ? force_segs : n_chunks <= IZG_RELAY_SPLIT8 ? 8 : 4);
+    ra.seg_blocks = (IZG_CHUNK_SIZE / 128) / ra.levels;
+    const uint64_t tasks = (uint64_t)n_chunks * ra.levels;
+    const uint32_t grid =
+        (uint32_t)std::min<uint64_t>((tasks + warps - 1) / warps, (uint64_t)rper_sm * rsms);
+    CUtensorMap omap;
+    std::memset(&omap, 0, sizeof(omap));
+    const int tma_out = IZG_TMA_STORE && make_out_map(&omap, d_out) ? 1 : 0;
+    rfn<<<grid, warps * 32, smem, rs>>>(d_words, d_chunks, n_chunks, d_out, d_status, d_consumed,
+                                        ra, omap, tma_out);
     return cudaGetLastError() == cudaSuccess ? IZG_SUCCESS : IZG_ERR_CUDA;
   }
   if (codec == IZG_SIMDBP128 && !probe && !split) {

@@ -61,8 +61,9 @@ def blocks(n, kind):
         low = rng.integers(0, 2**32, size=128, dtype=np.uint64)
         if kind == "overflow":      # 255 exceptions per block, one width: cursors pass 65,535,
             b, mb, c = 7, 19, 255   # 8 KiB of position bytes per 32 blocks
-        elif kind == "widths":      # every value an exception, widths 1..32 in turn: one
-            b, mb, c = 0, 1 + k % 32, 128   # super-iteration's packed groups exceed a window
+        elif kind == "widths":      # 100 exceptions per block, widths 1..32 in turn: most
+            b, mb, c = 0, 1 + k % 32, 100   # super-iterations need two groups per width (17.9 KB
+                                            # of packed groups, over a window), some one (9.5 KB)
         elif kind == "windows":     # several windows per page, all staged
             b = int(rng.integers(0, 12)); mb = b + int(rng.integers(1, 21)); c = int(rng.integers(20, 60))
         else:                       # sparse
