@@ -127,7 +127,7 @@ struct Slot {
   uint8_t* ws = nullptr;  // izg_decode_ws workspace (SIMD-FastPFOR index pass)
   uint64_t ws_cap = 0;
   cudaEvent_t decoded = nullptr;   // piece decoded: its D2H may start
-  cudaEvent_t drained[3] = {};     // piece's D2H parts done: the slot may be reused
+  cudaEvent_t drained[6] = {};     // piece's D2H parts done: the slot may be reused
 };
 
 struct Scratch {
@@ -136,8 +136,9 @@ struct Scratch {
   // device->host copies: each piece's output goes out as kParts concurrent
   // copies on kParts streams (several copies in flight keep D2H, the
   // pipeline's bottleneck, at ~56 GB/s instead of ~50 for one stream)
-  static constexpr int kParts = 3;
-  cudaStream_t d2h[kParts] = {};
+  static constexpr int kMaxParts = 6;
+  int kParts = 3;  // IZG_HOST_PARTS=1..6 (tuning knob)
+  cudaStream_t d2h[kMaxParts] = {};
   // pinned staging for the chunk table and the statuses, so every copy of
   // the pipeline is truly asynchronous (pageable copies block the host)
   izg_chunk* pin_table = nullptr;
@@ -214,8 +215,15 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
           cudaEventCreateWithFlags(&s.decoded, cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&s.drained[0], cudaEventDisableTiming) != cudaSuccess ||
           cudaEventCreateWithFlags(&s.drained[1], cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&s.drained[2], cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&s.drained[2], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s.drained[3], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s.drained[4], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&s.drained[5], cudaEventDisableTiming) != cudaSuccess)
         return IZG_ERR_CUDA;
+    if (const char* e = std::getenv("IZG_HOST_PARTS")) {
+      const int v = std::atoi(e);
+      if (v >= 1 && v <= Scratch::kMaxParts) S.kParts = v;
+    }
     for (auto& d : S.d2h)
       if (cudaStreamCreateWithFlags(&d, cudaStreamNonBlocking) != cudaSuccess) return IZG_ERR_CUDA;
   }
@@ -336,21 +344,27 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     runs.resize(m);
     if (runs.size() == 1) {  // contiguous: kParts concurrent copies keep D2H at ~56 GB/s
       const uint64_t r0 = runs[0].first, nout = runs[0].second;
-      const uint64_t part = (nout / Scratch::kParts + 1023) & ~uint64_t{1023};
+      static const uint64_t sub = [] {  // IZG_HOST_SUB_MI: copies of this many Mi integers
+        const char* e = std::getenv("IZG_HOST_SUB_MI");
+        const long v = e ? std::atol(e) : 0;
+        return (uint64_t)(v > 0 ? v : 0) << 20;
+      }();
+      const uint64_t part = sub ? sub : (nout / S.kParts + 1023) & ~uint64_t{1023};
       runs.clear();
-      for (int k = 0; k < Scratch::kParts; ++k) {
-        const uint64_t a = std::min<uint64_t>(nout, k * part);
-        const uint64_t b = k + 1 == Scratch::kParts ? nout : std::min<uint64_t>(nout, a + part);
-        if (b > a) runs.push_back({r0 + a, b - a});
+      for (uint64_t a = 0; a < nout; a += part)
+        runs.push_back({r0 + a, std::min<uint64_t>(part, nout - a)});
+      if (!sub && runs.size() > (size_t)S.kParts) {  // rounding left a sliver: fold it in
+        runs[S.kParts - 1].second += runs.back().second;
+        runs.pop_back();
       }
     }
-    for (int k = 0; k < Scratch::kParts; ++k) cudaStreamWaitEvent(S.d2h[k], s.decoded, 0);
+    for (int k = 0; k < S.kParts; ++k) cudaStreamWaitEvent(S.d2h[k], s.decoded, 0);
     for (size_t i = 0; i < runs.size(); ++i)
       cudaMemcpyAsync(h_out + olo + runs[i].first, s.out + runs[i].first, runs[i].second * 4,
-                      cudaMemcpyDeviceToHost, S.d2h[i % Scratch::kParts]);
+                      cudaMemcpyDeviceToHost, S.d2h[i % S.kParts]);
     cudaMemcpyAsync(st_host + c0, s.status, sizeof(int32_t) * nc, cudaMemcpyDeviceToHost,
                     S.d2h[0]);
-    for (int k = 0; k < Scratch::kParts; ++k) cudaEventRecord(s.drained[k], S.d2h[k]);
+    for (int k = 0; k < S.kParts; ++k) cudaEventRecord(s.drained[k], S.d2h[k]);
   }
   for (auto& s : S.slot)
     if (cudaStreamSynchronize(s.stream) != cudaSuccess) rc = IZG_ERR_CUDA;

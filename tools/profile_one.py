@@ -10,6 +10,7 @@ CFG = {
     "c1big": ("simdbp128-s4", "cluster", 8192, 29, 0, False),
     "raw0": ("simdbp128", "raw", 4096, 0, 0, True),
     "raw16": ("simdbp128", "raw", 4096, 16, 0, True),
+    "c3": ("simdbp128-s4", "uniform", 4096, 26, 0, False),
     "c4": ("simdfastpfor-s4", "geometric", 2048, 32, 100000, False),
     "c5fp": ("simdfastpfor-s4", "cluster", 8192, (20, 29), 0, False),
     "c5bp": ("simdbp128-s4", "cluster", 8192, (20, 29), 0, False),
