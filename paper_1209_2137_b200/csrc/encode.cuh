@@ -273,25 +273,47 @@ __global__ void __launch_bounds__(kEncWarps * 32)
 #pragma unroll
               for (int j = 0; j < 4; ++j) atomicAdd(&sc.hist[q][bitw(d[k][j])], 1u);
           __syncwarp();
-          if (s8 == 0 && live) {
-            // fastpfor_choose_width: argmin over b of b*128 + (8+maxbits-b)*c(b)
-            uint32_t maxbits = 0;
-            for (uint32_t w = 0; w <= 32; ++w)
-              if (sc.hist[q][w]) maxbits = w;
-            uint32_t above = 0, best_b = maxbits, best_c = 0;
-            uint64_t best = ~uint64_t{0};
-            for (int b = 32; b >= 0; --b) {
-              if ((uint32_t)b <= maxbits) {
-                const uint64_t cost = (uint64_t)b * 128 + (above ? (uint64_t)(8 + maxbits - b) * above : 0);
-                if (cost < best) {  // scanning downward: strict keeps the larger b on ties
-                  best = cost;
-                  best_b = b;
-                  best_c = above;
-                }
-              }
-              above += sc.hist[q][b];
+          {
+            // fastpfor_choose_width (codec_patched.cpp:33-48): argmin over b <= maxbits of
+            // b*128 + (8+maxbits-b)*c(b), c(b) = values wider than b, ties toward the larger
+            // b.  The block's eight lanes each take four candidates b = 4*s8 .. 4*s8+3 (lane
+            // 7 also b = 32): c(b) is a suffix sum of the histogram (four bins per lane, an
+            // 8-lane suffix scan), the winner an 8-lane min of cost << 14 | (63-b) << 8 | c.
+            const uint32_t* h = sc.hist[q];
+            const uint32_t h0 = h[4 * s8], h1 = h[4 * s8 + 1], h2 = h[4 * s8 + 2],
+                           h3 = h[4 * s8 + 3], h32 = h[32];
+            uint32_t orv = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) orv |= d[k][0] | d[k][1] | d[k][2] | d[k][3];
+            orv |= __shfl_xor_sync(0xFFFFFFFFu, orv, 1);
+            orv |= __shfl_xor_sync(0xFFFFFFFFu, orv, 2);
+            orv |= __shfl_xor_sync(0xFFFFFFFFu, orv, 4);
+            const uint32_t maxbits = bitw(orv);
+            const uint32_t tot = h0 + h1 + h2 + h3;
+            uint32_t incl = tot;
+#pragma unroll
+            for (int dd = 1; dd < 8; dd <<= 1) {
+              const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, incl, dd, 8);
+              if (s8 + dd < 8) incl += y;
             }
-            sc.tab[g0 + q] = best_b | maxbits << 6 | best_c << 12;
+            uint32_t above[4];
+            above[3] = incl - tot + h32;  // values wider than 4*s8+3
+            above[2] = above[3] + h3;
+            above[1] = above[2] + h2;
+            above[0] = above[1] + h1;
+            uint32_t key = 0xFFFFFFFFu;
+#pragma unroll
+            for (uint32_t i = 0; i < 4; ++i) {
+              const uint32_t b = 4 * s8 + i;
+              const uint32_t cost = b * 128u + (8u + maxbits - b) * above[i];
+              if (b <= maxbits) key = min(key, cost << 14 | (63u - b) << 8 | above[i]);
+            }
+            if (maxbits == 32) key = min(key, (32u * 128u) << 14 | (63u - 32u) << 8);
+            key = min(key, __shfl_xor_sync(0xFFFFFFFFu, key, 1));
+            key = min(key, __shfl_xor_sync(0xFFFFFFFFu, key, 2));
+            key = min(key, __shfl_xor_sync(0xFFFFFFFFu, key, 4));
+            if (s8 == 0 && live)
+              sc.tab[g0 + q] = (63u - ((key >> 8) & 63u)) | maxbits << 6 | (key & 0xFFu) << 12;
           }
           __syncwarp();
         }

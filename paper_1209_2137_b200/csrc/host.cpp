@@ -349,7 +349,8 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
         const long v = e ? std::atol(e) : 0;
         return (uint64_t)(v > 0 ? v : 0) << 20;
       }();
-      const uint64_t part = sub ? sub : (nout / S.kParts + 1023) & ~uint64_t{1023};
+      const uint64_t part =
+          sub ? sub : std::max<uint64_t>(1024, (nout / S.kParts + 1023) & ~uint64_t{1023});
       runs.clear();
       for (uint64_t a = 0; a < nout; a += part)
         runs.push_back({r0 + a, std::min<uint64_t>(part, nout - a)});
