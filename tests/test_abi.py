@@ -140,6 +140,26 @@ def test_decode_argument_validation():
     assert L.izg_decode(0, 2, None, None, 0, None, None, None, None) == N.SUCCESS
 
 
+def test_workspace_sizes_by_batch():
+    """izg_decode_workspace_size (a host-side function): SIMD-BP128 asks for the
+    split kernel's states on small batches, for the relay kernel's 64 bytes per
+    chunk (+ the task counter) from 2,432 to 14,208 chunks and for nothing
+    elsewhere; SIMD-FastPFOR always asks for at least its page index."""
+    env = {k: os.environ.get(k) for k in ("IZG_RELAY", "IZG_SPLIT")}
+    if any(v is not None for v in env.values()):
+        pytest.skip("forced decode paths in the environment")
+    L = N.lib()
+    bp, fp = P.make_codec("simdbp128-s4").codec, P.make_codec("simdfastpfor-s4").codec
+    assert L.izg_decode_workspace_size(bp, 64) > 0            # split
+    assert L.izg_decode_workspace_size(bp, 1024) == 0         # CTA kernel: no workspace
+    assert L.izg_decode_workspace_size(bp, 2431) == 0
+    for n in (2432, 4096, 14208):
+        assert L.izg_decode_workspace_size(bp, n) == 64 * n + 64
+    assert L.izg_decode_workspace_size(bp, 14209) == 0
+    for n in (64, 4096, 65536):
+        assert L.izg_decode_workspace_size(fp, n) >= L.izg_decode_index_workspace_size(fp, n) > 0
+
+
 def test_checksum_host_matches_numpy():
     import harness as H
     from paper_1209_2137_b200.device import host_checksum
