@@ -149,3 +149,14 @@ def test_relay_default_routing_ragged_batch(cuda):
         assert np.array_equal(a.statuses(), sb), rep
         assert np.array_equal(a.output()[good], ob[good]), rep
         assert np.array_equal(a.consumed[:count].cpu().numpy(), b.consumed[:count].cpu().numpy())
+
+
+@pytest.mark.parametrize("env", [{}, {"IZG_RELAY": "1", "IZG_SPLIT": "0", "IZG_CTA": "0"}])
+def test_relay_randomized_stress_short(cuda, env):
+    """tools/relay_stress.py for 15 s: random batch sizes, ragged lengths, delta modes and
+    the raw mode, bit flips and truncated payloads, against the one-warp kernel (a
+    10-minute run: profiles/r02_relay_stress.log, 1.06 M chunks)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "relay_stress.py"), "15", "7"],
+                       cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().startswith("ok:"), r.stdout[-1000:] + r.stderr[-3000:]
