@@ -179,7 +179,10 @@ int izg_decode(int codec, int delta, const uint32_t* d_words,
  * table-driven decode).  Small batches of SIMD-BP128 or SIMD-FastPFOR add
  * the split decode's look-back state (several warps per chunk, decoupled
  * look-back carry; IZG_SPLIT=0/1 in the environment forces it off/on).
- * 0 when nothing applies. */
+ * SIMD-BP128 batches of 2,432..14,208 chunks ask for the relay decode's
+ * per-chunk state (64 bytes per chunk + 64: segments of a chunk claimed level
+ * by level, position / carry / first error handed on in order; IZG_RELAY=0/1
+ * forces it off/on).  0 when nothing applies. */
 uint64_t izg_decode_workspace_size(int codec, uint32_t n_chunks);
 
 /* The page index alone (SIMD-FastPFOR; 0 otherwise): a workspace of exactly
