@@ -449,6 +449,8 @@ int decode_impl(int codec, int delta, const uint32_t* d_words, const izg_chunk* 
     ra.st = static_cast<RelayState*>(d_ws);
     ra.next_task = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(d_ws) +
                                                relay_state_bytes(n_chunks));
+    ra.summary = reinterpret_cast<unsigned long long*>(static_cast<uint8_t*>(d_ws) +
+                                                       relay_state_bytes(n_chunks) + 8);
     ra.levels = (uint32_t)(force_segs ? force_segs : n_chunks <= IZG_RELAY_SPLIT8 ? 8 : 4);
     ra.seg_blocks = (IZG_CHUNK_SIZE / 128) / ra.levels;
     const uint64_t tasks = (uint64_t)n_chunks * ra.levels;

@@ -294,7 +294,12 @@ extern "C" int izg_decode_host(int codec, int delta, const uint32_t* h_words, ui
     const uint64_t wcopy = std::min<uint64_t>(n_words, (whi + 3) & ~uint64_t{3}) - wlo;
     const uint64_t wneed = ((whi + 3) & ~uint64_t{3}) - wlo + 4;  // + the contract's pad row
     uint64_t tcap = s.table_cap;
-    const uint64_t wsb = izg_decode_workspace_size(codec, nc);
+    // SIMD-BP128 pieces never take the relay kernel here: it pays for chunks of tens of
+    // thousands of integers at 2,432+ chunks per launch, and a piece (at most 64 Mi
+    // integers) with that many chunks holds short ones, where it costs 5-15 %
+    // (tools/relay_short.py).  Small pieces keep the split kernel's workspace.
+    const uint64_t wsb =
+        codec == IZG_SIMDBP128 && nc >= 2432 ? 0 : izg_decode_workspace_size(codec, nc);
     if (!grow(s.words, s.words_cap, wneed) || !grow(s.table, tcap, nc) ||
         !grow(s.out, s.out_cap, std::max<uint64_t>(ohi - olo, 1)) ||
         (wsb && !grow(s.ws, s.ws_cap, wsb))) {

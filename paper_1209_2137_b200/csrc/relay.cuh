@@ -36,6 +36,7 @@ struct RelayState {
 struct RelayArgs {
   RelayState* st;       // one per chunk, zeroed
   uint32_t* next_task;  // zeroed
+  unsigned long long* summary;  // zeroed; see the kernel
   uint32_t seg_blocks;  // blocks per segment, a multiple of 16 (whole meta-blocks)
   uint32_t levels;      // segments of a full chunk
 };
@@ -83,8 +84,31 @@ __global__ void __launch_bounds__((Layout<(DELTA >= 0 ? IZG_SIMDBP128 : 0)>::kWa
     const izg_chunk ch = chunks[c];
     const uint32_t core = kArray ? ch.n / 128 * 128 : ch.n;
     const uint32_t nblocks = core / 128;
-    const uint32_t nseg = nblocks ? (nblocks + SB - 1) / SB : 1u;
-    if (k >= nseg) continue;
+    // segments of this chunk: SB blocks each, the last one takes what is left (raw-mode
+    // chunks may hold more than 65,536 integers: more blocks than levels * SB)
+    const uint32_t nseg = nblocks ? min(ra.levels, (nblocks + SB - 1) / SB) : 1u;
+    if (k == 0 && lane == 0) {
+      // batch summary, one 64-bit word: low half = level-0 tasks seen, high half bit j =
+      // some chunk has a segment j.  Both updates hit one address from one thread, so the
+      // count never runs ahead of the bits it vouches for (no fence needed).
+      const uint32_t sbits = (nseg >= 32 ? 0xFFFFFFFFu : (1u << nseg) - 1u) & ~1u;
+      if (sbits) atomicOr(ra.summary, (unsigned long long)sbits << 32);
+      atomicAdd(ra.summary, 1ull);
+    }
+    if (k >= nseg) {
+      // every chunk's first task has been seen and none has a segment k: nor has any
+      // later task (levels only grow), so this warp is done — batches of short chunks
+      // do not pay for claiming and skipping the upper levels
+      // (level-0 tasks post the summary first thing, so the wait below is a microsecond
+      // at the start of the launch and nothing afterwards; bounded like every spin here)
+      unsigned long long sm = ld_relaxed64(ra.summary);
+      for (uint32_t spins = 0; (uint32_t)sm != n_chunks && spins < 4096; ++spins) {
+        __nanosleep(128);
+        sm = ld_relaxed64(ra.summary);
+      }
+      if ((uint32_t)sm == n_chunks && !((sm >> (32 + k)) & 1ull)) break;
+      continue;
+    }
     int32_t st = precheck(IZG_SIMDBP128, kArray, ch.n);
     if (st != IZG_OK) {  // every task of the chunk sees it; task 0 reports
       if (k == 0 && lane == 0) {

@@ -18,12 +18,14 @@ class DeviceBatch:
     runs izg_decode_ws's two-launch path (page index pass + table-driven
     decode); indexed=False keeps the single fused launch of izg_decode.
     materialize=False allocates no output (for decode_intersect_device).
+    relay_long_only=False keeps the SIMD-BP128 relay workspace for batches of short
+    chunks too (tests).
     split=False sizes the workspace for the page index only, so small batches
     keep one warp per chunk instead of the split kernel (csrc/split.cuh)."""
 
     def __init__(self, codec: Codec, enc: Encoded, device=None, *, raw: bool = False,
                  out=None, indexed: bool = True, materialize: bool = True,
-                 split: bool = True):
+                 split: bool = True, relay_long_only: bool = True):
         import torch
 
         self.torch = torch
@@ -52,6 +54,12 @@ class DeviceBatch:
         if indexed:
             ws = (L.izg_decode_workspace_size(codec.codec, self.n_chunks) if split
                   else L.izg_decode_index_workspace_size(codec.codec, self.n_chunks))
+            # SIMD-BP128 batches of 2,432+ chunks: the workspace selects the relay kernel,
+            # which pays for long chunks only (4-12 % at 65,536 integers per chunk, 5-15 %
+            # lost on chunks of a few thousand: tools/relay_short.py)
+            if (relay_long_only and codec.codec == N.SIMDBP128 and self.n_chunks >= 2432
+                    and self.n_out < 32768 * self.n_chunks):
+                ws = 0
         self.workspace = (torch.empty(ws, dtype=torch.uint8, device=self.device)
                           if ws else None)
 

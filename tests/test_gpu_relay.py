@@ -44,6 +44,7 @@ for name in ["simdbp128", "simdbp128-s4", "simdbp128-d2", "simdbp128-dm"]:
 for name in ["simdbp128", "simdbp128-s4"]:
     T.test_reference_encoded_buffers_decode(torch, R, name)
     T.test_mutation_fuzz_accept_reject_matches_reference(torch, R, name)
+RL.raw_chunks_longer_than_the_levels()
 T.test_decode_deltas_every_width(torch, R, "simdbp128")
 T.test_device_batch_consumed_words(torch, R)
 T.test_chunk_length_and_count_errors(torch)
@@ -95,6 +96,28 @@ def corruption_vs_one_warp(name, trials=25):
             assert np.array_equal(oa[lo:lo + n], ob[lo:lo + n]), (name, trial, c)
 
 
+def raw_chunks_longer_than_the_levels():
+    """Codec-level (raw) SIMD-BP128 chunks may hold more than 65,536 integers, i.e. more
+    blocks than levels x segment size: the last level takes the remainder.  Against the
+    one-warp kernel and the input (called inside the forced subprocess)."""
+    codec = P.make_codec("simdbp128")
+    rng = np.random.default_rng(31)
+    lens = np.array([128 * 3000, 128 * 513, 65536, 128 * 1025, 128, 128 * 7], np.uint32)
+    offs = np.concatenate([[0], np.cumsum(lens, dtype=np.uint64)[:-1]]).astype(np.uint64)
+    flat = rng.integers(0, 1 << 13, size=int(lens.sum()), dtype=np.uint32)
+    flat[::977] = rng.integers(0, 2**32, size=len(flat[::977]), dtype=np.uint64).astype(np.uint32)
+    enc = H.encode_chunks(codec, flat, offs, lens, raw=True)
+    a = P.DeviceBatch(codec, enc, raw=True)
+    b = P.DeviceBatch(codec, enc, raw=True, indexed=False)
+    assert a.workspace is not None
+    a.decode()
+    b.decode()
+    a.check()
+    b.check()
+    assert np.array_equal(a.output(), flat) and np.array_equal(b.output(), flat)
+    assert np.array_equal(a.consumed[:len(lens)].cpu().numpy(), b.consumed[:len(lens)].cpu().numpy())
+
+
 @pytest.mark.parametrize("segs", [2, 4, 8, 32])
 def test_relay_kernel_parity_suite(cuda, segs):
     _run({"IZG_RELAY": "1", "IZG_SPLIT": "0", "IZG_RELAY_SEGS": str(segs)},
@@ -132,8 +155,9 @@ def test_relay_default_routing_ragged_batch(cuda):
         off, nw = int(enc.table["word_off"][c]), int(enc.table["n_words"][c])
         w[off + int(rng.integers(0, nw))] ^= np.uint32(1) << np.uint32(rng.integers(0, 32))
     bad = Encoded(w, enc.table)
-    a = P.DeviceBatch(codec, bad)
+    a = P.DeviceBatch(codec, bad, relay_long_only=False)
     b = P.DeviceBatch(codec, bad, indexed=False)
+    assert a.workspace is not None
     b.decode()
     sb, ob = b.statuses(), b.output()
     assert (sb == 0).sum() >= count - 64
@@ -160,3 +184,24 @@ def test_relay_randomized_stress_short(cuda, env):
                        cwd=ROOT, env=dict(os.environ, **env), capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().startswith("ok:"), r.stdout[-1000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("n", [1, 100, 1000, 8192 + 5])
+def test_relay_default_routing_short_chunks(cuda, n):
+    """Batches of short chunks in the relay's default range: every chunk has one segment
+    (or two), the warps leave at the first task of a level no chunk reaches."""
+    codec = P.make_codec("simdbp128-s4")
+    count = 5000
+    rng = np.random.default_rng(n)
+    flat = np.cumsum(rng.integers(0, 64, size=(count, n), dtype=np.uint32), axis=1,
+                     dtype=np.uint32).reshape(-1)
+    offs = np.arange(count, dtype=np.uint64) * n
+    enc = H.encode_chunks(codec, flat, offs, np.full(count, n, np.uint32))
+    assert P.DeviceBatch(codec, enc).workspace is None  # short chunks: one warp per chunk
+    b = P.DeviceBatch(codec, enc, relay_long_only=False)
+    assert b.workspace is not None
+    for _ in range(3):
+        b.out.fill_(0)
+        b.decode()
+        b.check()
+        assert np.array_equal(b.output(), flat)

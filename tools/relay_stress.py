@@ -50,7 +50,7 @@ while time.time() < t_end:
         if table["n_words"][c] > 1:
             table["n_words"][c] = int(rng.integers(0, int(table["n_words"][c])))
     bad = Encoded(w, table)
-    a = P.DeviceBatch(codec, bad, raw=raw)
+    a = P.DeviceBatch(codec, bad, raw=raw, relay_long_only=False)
     b = P.DeviceBatch(codec, bad, raw=raw, indexed=False)
     assert a.workspace is not None, count
     b.decode(); torch.cuda.synchronize()
